@@ -1,0 +1,18 @@
+"""B200-native certified quantized decode attention (arXiv 2605.20868).
+
+Drop-in for the reference ``certkv`` hot path: cache append / quantize, the
+certified attention call, the bound report and the fallback ladder, backed by
+hand-written sm_100a CUDA kernels behind the C ABI in include/certkv_b200.h.
+"""
+
+__version__ = "0.1.0"
+
+from . import _lib, kernels
+from .cache import (DeviceKVCache, ScratchCache, StorageReport, TieredCache, storage_report,
+                    storage_table)
+from .engine import (CertifiedDecoder, HeadStepResult, StepOutput, dense_attention,
+                     run_decode_step)
+from .errors import EmptyCacheError, PagingError, Tier2UnavailableError
+from .harness import (RunResult, Workload, WorkloadConfig, aggregate_telemetry,
+                      generate_workload, gqa_union, run_workload)
+from .policy import Certificate, FallbackEvent, PolicyConfig, RungFlags

@@ -1,0 +1,142 @@
+// extern "C" entry points of libcertkv_b200.so (declared in include/certkv_b200.h).
+#include "common.cuh"
+
+namespace ckv {
+extern int g_launches;
+cudaError_t launch_append(const ckv_cache*, const uint16_t*, const uint16_t*, int32_t, cudaStream_t);
+cudaError_t launch_read_tier1(const ckv_cache*, int, int, int, int8_t*, float*, float*, uint8_t*,
+                              uint16_t*, uint16_t*, cudaStream_t);
+cudaError_t launch_fault_offset(const ckv_cache*, int, int, int, float, cudaStream_t);
+cudaError_t launch_tier2_drop(const ckv_cache*, int, int, cudaStream_t);
+cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
+cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
+cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
+int lru_ring(int, int);
+cudaError_t launch_block_logmass(const double*, const int64_t*, int, double*, double*, double*,
+                                 cudaStream_t);
+cudaError_t launch_fused_attend(const float*, const float*, const int64_t*, int, int, float*, float*,
+                                cudaStream_t);
+}  // namespace ckv
+
+static ckv_status st_of(cudaError_t e) { return e == cudaSuccess ? CKV_OK : CKV_ECUDA; }
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static bool cache_ok(const ckv_cache* c) {
+  return c && c->n_units > 0 && c->max_blocks > 0 && c->tier1 && c->eta && c->nu && c->kscale_max &&
+         c->v_max && c->n_blocks && c->partial_len && c->partial_k && c->partial_v && c->tier2_k &&
+         c->tier2_v && c->tier2_valid && c->status;
+}
+
+extern "C" {
+
+int32_t ckv_version(void) { return 100; }
+
+int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity) {
+  return 4 + max_blocks + ckv::lru_ring(max_blocks, capacity);
+}
+
+ckv_status ckv_scratch_init(int32_t n_units, int32_t max_blocks, const ckv_scratch* sc,
+                            void* stream) {
+  if (!sc || n_units <= 0 || max_blocks <= 0 || sc->key_capacity < 0 || sc->value_capacity < 0 ||
+      !sc->key_lru || !sc->value_lru || !sc->counters)
+    return CKV_EINVAL;
+  cudaError_t e = ckv::launch_lru_init(sc->key_lru, n_units, max_blocks, sc->key_capacity, S(stream));
+  if (e == cudaSuccess)
+    e = ckv::launch_lru_init(sc->value_lru, n_units, max_blocks, sc->value_capacity, S(stream));
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(sc->counters, 0, sizeof(int64_t) * 6 * (size_t)n_units, S(stream));
+  return st_of(e);
+}
+
+ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const ckv_policy* pol,
+                    ckv_step* st) {
+  if (!pol || !st || n_units <= 0 || max_blocks <= 0 || n_heads < 1 || n_heads > CKV_MAX_QHEADS)
+    return CKV_EINVAL;
+  if (pol->k_max < 0 || pol->k_min < 0 || pol->k_max < pol->k_min || pol->k_max > 511 ||
+      pol->ranking_depth < 1 || pol->ranking_depth > 64)
+    return CKV_EINVAL;
+  long long work = (long long)n_units * max_blocks / 1184;
+  int bps = 128;
+  while (bps > 16 && bps > work) bps >>= 1;
+  st->n_heads = n_heads;
+  st->blocks_per_split = bps;
+  st->n_splits = (max_blocks + bps - 1) / bps;
+  st->kcap = 2 * pol->k_max + 2;
+  st->wcap = st->kcap + max_blocks;
+  st->items_per_chunk = 32;
+  st->n_chunks = (st->kcap + 31) / 32;
+  if (st->n_chunks < 1) st->n_chunks = 1;
+  return CKV_OK;
+}
+
+ckv_status ckv_append(const ckv_cache* c, const uint16_t* k_new, const uint16_t* v_new,
+                      int32_t n_tok, void* stream) {
+  if (!cache_ok(c) || n_tok < 0 || (n_tok > 0 && (!k_new || !v_new))) return CKV_EINVAL;
+  if (n_tok == 0) return CKV_OK;
+  return st_of(ckv::launch_append(c, k_new, v_new, n_tok, S(stream)));
+}
+
+ckv_status ckv_reset(const ckv_cache* c, void* stream) {
+  if (!cache_ok(c)) return CKV_EINVAL;
+  return st_of(ckv::launch_reset(c, S(stream)));
+}
+
+ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                           const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+  if (!cache_ok(c) || !pol || !st || !st->q || !st->out || !st->cert || !st->lm1 ||
+      !st->split_state || !st->order || !st->work || !st->n_work || !st->vlist || !st->lm2 ||
+      !st->head_state || !st->chunk_state)
+    return CKV_EINVAL;
+  if (host_max_blocks < 0 || host_max_blocks > c->max_blocks) return CKV_EINVAL;
+  if (pol->greedy_value_budget >= 0.0) return CKV_EINVAL;  // greedy rung 2 not on device yet
+  cudaError_t e = ckv::launch_decode(c, pol, st, host_max_blocks, S(stream));
+  if (e != cudaSuccess) return CKV_ECUDA;
+  if (scratch) {
+    if (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters)
+      return CKV_EINVAL;
+    e = ckv::launch_scratch(c, st, scratch, S(stream));
+    if (e != cudaSuccess) return CKV_ECUDA;
+  }
+  return CKV_OK;
+}
+
+ckv_status ckv_read_tier1(const ckv_cache* c, int32_t unit, int32_t b0, int32_t nb, int8_t* kcodes,
+                          float* kscale, float* koffset, uint8_t* vcodes, uint16_t* vscale,
+                          uint16_t* voffset, void* stream) {
+  if (!cache_ok(c) || unit < 0 || unit >= c->n_units || b0 < 0 || nb < 0 || b0 + nb > c->max_blocks)
+    return CKV_EINVAL;
+  return st_of(ckv::launch_read_tier1(c, unit, b0, nb, kcodes, kscale, koffset, vcodes, vscale,
+                                      voffset, S(stream)));
+}
+
+ckv_status ckv_fault_offset(const ckv_cache* c, int32_t unit, int32_t block, int32_t channel,
+                            float shift, void* stream) {
+  if (!cache_ok(c) || unit < 0 || unit >= c->n_units || block < 0 || block >= c->max_blocks ||
+      channel < 0 || channel >= CKV_HEAD_DIM)
+    return CKV_EINVAL;
+  return st_of(ckv::launch_fault_offset(c, unit, block, channel, shift, S(stream)));
+}
+
+ckv_status ckv_tier2_drop(const ckv_cache* c, int32_t unit, int32_t block, void* stream) {
+  if (!cache_ok(c) || unit < 0 || unit >= c->n_units || block < 0 || block >= c->max_blocks)
+    return CKV_EINVAL;
+  return st_of(ckv::launch_tier2_drop(c, unit, block, S(stream)));
+}
+
+ckv_status ckv_block_logmass(const double* scores, const int64_t* bounds, int32_t nb,
+                             double* block_max, double* block_sum, double* log_mass, void* stream) {
+  if (nb < 0 || (nb > 0 && (!scores || !bounds || !block_max || !block_sum || !log_mass)))
+    return CKV_EINVAL;
+  return st_of(ckv::launch_block_logmass(scores, bounds, nb, block_max, block_sum, log_mass, S(stream)));
+}
+
+ckv_status ckv_fused_attend(const float* scores, const float* values, const int64_t* bounds,
+                            int32_t nb, int32_t d, float* out, float* ml, void* stream) {
+  if (nb < 0 || d <= 0 || d > 1024 || !out || !ml) return CKV_EINVAL;
+  return st_of(ckv::launch_fused_attend(scores, values, bounds, nb, d, out, ml, S(stream)));
+}
+
+int32_t ckv_last_launches(void) { return ckv::g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// Shared device helpers and the Tier-1 block record layout.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "certkv_b200.h"
+
+namespace ckv {
+
+constexpr int D = CKV_HEAD_DIM;     // 128
+constexpr int B = CKV_BLOCK;        // 16
+constexpr int G = CKV_GROUP;        // 16
+constexpr int NG = D / G;           // 8 value groups
+constexpr int H = CKV_MAX_QHEADS;   // 4
+constexpr int REC = CKV_BLOCK_BYTES;
+
+// Tier-1 block record (4608 B, one contiguous bulk copy):
+//   [   0, 2048) key codes int8, mma.m16n8k32 A-fragment order:
+//                for k-tile kt (32 channels) and lane l: 16 bytes =
+//                {row l/4 cols 4(l%4)+0..3, row l/4+8 same cols,
+//                 row l/4 cols 16+4(l%4)+0..3, row l/4+8 same cols}
+//   [2048, 2560) key scale  f32[128]
+//   [2560, 3072) key offset f32[128]
+//   [3072, 4096) value codes: [half h][lane l][token 8h+i] u16 holding the
+//                nibbles of channels 4l..4l+3 (channel 4l+j at bits 4j)
+//   [4096, 4608) value meta: [group g][token t] half2(scale, offset)
+constexpr int OFF_KCODES = 0;
+constexpr int OFF_KSCALE = 2048;
+constexpr int OFF_KOFF = 2560;
+constexpr int OFF_VCODES = 3072;
+constexpr int OFF_VMETA = 4096;
+
+__host__ __device__ inline int kcode_offset(int t, int c) {
+  int kt = c >> 5, cc = c & 31;
+  int lane = (t & 7) * 4 + ((cc & 15) >> 2);
+  int reg = (t >> 3) + 2 * (cc >> 4);
+  return OFF_KCODES + kt * 512 + lane * 16 + reg * 4 + (cc & 3);
+}
+__host__ __device__ inline int vcode_offset(int t, int c) {  // byte holding channel c's nibble pair
+  int l = c >> 2;
+  return OFF_VCODES + (t >> 3) * 512 + l * 16 + (t & 7) * 2 + ((c & 3) >> 1);
+}
+__host__ __device__ inline int vmeta_offset(int t, int g) { return OFF_VMETA + (g * 16 + t) * 4; }
+
+// ---- bit helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+__device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+
+// Correctly rounded float64 -> binary16 (round to nearest even), matching
+// numpy's astype(float16) from float64 (no double rounding through fp32).
+__device__ inline uint16_t double_to_half_rn(double x) {
+  uint16_t sign = signbit(x) ? 0x8000 : 0;
+  double a = fabs(x);
+  if (isnan(a)) return 0x7e00;
+  if (a >= 65520.0) return sign | 0x7c00;  // rounds to inf
+  if (a < 6.103515625e-05) {                // subnormal range: units of 2^-24
+    double q = rint(a * 16777216.0);        // exact scaling by a power of two
+    return sign | (uint16_t)q;              // q <= 1024 -> 1024 is the min normal
+  }
+  int e;
+  double m = frexp(a, &e);                  // a = m * 2^e, m in [0.5, 1)
+  double q = rint(ldexp(m, 11));            // 11 significant bits
+  if (q >= 2048.0) { q *= 0.5; e += 1; }
+  if (e - 1 + 15 >= 31) return sign | 0x7c00;
+  uint16_t exp_bits = (uint16_t)(e - 1 + 15);
+  uint16_t man = (uint16_t)((int)q - 1024);
+  return sign | (uint16_t)(exp_bits << 10) | man;
+}
+
+__device__ __forceinline__ double half_bits_to_double(uint16_t h) {
+  return (double)__half2float(__ushort_as_half(h));
+}
+
+// ---- warp reductions ----------------------------------------------------------
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- mbarrier + bulk async copy (TMA 1-D) -------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, "
+      "p;\n}" : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ---- integer MMA: D(16x8,s32) += A(16x32,s8) * B(32x8,u8) ---------------------
+__device__ __forceinline__ void mma_s8u8(int (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// exp via exp2 with a pre-scaled argument
+__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+}  // namespace ckv

@@ -1,0 +1,1043 @@
+// The certified decode step on device.
+//
+//   pass A  (k_pass_a)  streams every unit's Tier-1 once (TMA bulk copies into
+//                       a per-warp smem ring): Phase-1 INT8 scores on the
+//                       tensor cores, per-block log-mass l'_b, Delta_b, and a
+//                       *speculative* Phase-2 online-softmax attend over all
+//                       blocks with quantized scores and INT4 values.
+//   select  (k_select)  per q-head: lse, radix top-K, coverage K*, Rung 1,
+//                       tail mass, Rung 2 value promotions, tail part of
+//                       E_val, the promoted / value work list.
+//   pass B  (k_pass_b)  per q-head over the work list only: original-key
+//                       scores from Tier-2, phase-2 log-mass of promoted
+//                       blocks, canary gap, and the additive correction that
+//                       turns the speculative attend into the mask-gated one.
+//   combine (k_combine) per q-head: merge, output, ranking / boundary /
+//                       canary monitors, E_key / E_val, rung flags.
+//
+// Every additive decomposition is over blocks, so the result equals the
+// reference's single mask-gated pass (attention.py:227-300) up to fp32
+// rounding.
+#include "phase1.cuh"
+
+namespace ckv {
+
+struct HeadState {
+  double lse;          // phase-1 log-sum-exp over full blocks + partial
+  double alpha_hat;    // estimated tail mass (non-promoted full blocks)
+  double e_tail;       // sum over b not in F u V of p_b eta_b
+  double partial_mass;
+  float mA, lA;        // merged pass-A softmax state
+  float delta;         // Delta_h
+  float tailmax;       // max phase-1 log-mass over the tail (-inf if empty)
+  float mp, lp;        // partial block state
+  int32_t kprime;      // |F| after rung 1
+  int32_t kstar0;      // K* before rung 1
+  int32_t n_v;
+  int32_t k_cov;
+  int32_t pad[2];
+  float oA[D];
+  float np_[D];
+};
+static_assert(sizeof(HeadState) <= CKV_HEAD_FLOATS * 4, "head state too large");
+
+struct StepArgs {
+  ckv_cache c;
+  ckv_step st;
+  ckv_policy pol;
+};
+
+__device__ __forceinline__ float ninf() { return __int_as_float(0xff800000); }
+
+__device__ __forceinline__ uint32_t okey(float x) {  // order-preserving float -> u32
+  uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// =============================================================================
+// pass A
+// =============================================================================
+constexpr int PA_WARPS = 4;
+constexpr int PA_STAGES = 3;
+
+struct PassASmem {
+  uint8_t stage[PA_WARPS][PA_STAGES][REC];
+  uint64_t bar[PA_WARPS][PA_STAGES];
+  float qh[H * D];
+  float pbuf[PA_WARPS][B][H];
+  float abuf[PA_WARPS][H];
+};
+
+__global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const int u = blockIdx.y, sp = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nh = st.n_heads;
+  const int nb = c.n_blocks[u];
+  const int b0 = sp * st.blocks_per_split;
+  const int b1 = min(nb, b0 + st.blocks_per_split);
+  const float inv_sqrt_d = 0.08838834764831845f;
+
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    int h = i / D;
+    S.qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845)
+                       : 0.f;
+  }
+  if (tid == 0) {
+    for (int w = 0; w < PA_WARPS; ++w)
+      for (int s = 0; s < PA_STAGES; ++s) mbar_init(&S.bar[w][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  (void)inv_sqrt_d;
+
+  QFrag f;
+  load_qfrag(f, S.qh, lane);
+
+  const int span = b1 - b0;
+  const int nmine = (span > warp) ? (span - warp + PA_WARPS - 1) / PA_WARPS : 0;
+  const uint8_t* ubase = c.tier1 + (size_t)u * c.max_blocks * REC;
+  const float* smax_u = c.kscale_max + (size_t)u * c.max_blocks;
+  if (lane == 0) {
+    for (int s = 0; s < PA_STAGES && s < nmine; ++s) {
+      int b = b0 + warp + PA_WARPS * s;
+      mbar_expect_tx(&S.bar[warp][s], REC);
+      bulk_g2s(S.stage[warp][s], ubase + (size_t)b * REC, REC, &S.bar[warp][s]);
+    }
+  }
+
+  const int h = lane & 3;
+  const int t0 = lane >> 2, t1 = t0 + 8;
+  float m_run = ninf(), l_run = 0.f, dmax = 0.f;
+  float o[H][4];
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[i][j] = 0.f;
+
+  float* lm1 = st.lm1 + ((size_t)u * nh + (h < nh ? h : 0)) * c.max_blocks;
+  const int g = lane >> 2;  // value group of the lane's channels
+
+  for (int i = 0; i < nmine; ++i) {
+    const int s = i % PA_STAGES;
+    const uint32_t par = (uint32_t)(i / PA_STAGES) & 1u;
+    const int b = b0 + warp + PA_WARPS * i;
+    const float smax = __ldg(smax_u + b);
+    mbar_wait(&S.bar[warp][s], par);
+    const uint8_t* rec = S.stage[warp][s];
+
+    // ---- phase 1: scores, block statistics --------------------------------
+    BlockScores r = phase1_block(f, rec, smax, lane);
+    float bm = fmaxf(r.s0, r.s1);
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+    const float e0 = fast_exp(r.s0 - bm), e1 = fast_exp(r.s1 - bm);
+    float bs = e0 + e1;
+    bs += __shfl_xor_sync(0xffffffffu, bs, 4);
+    bs += __shfl_xor_sync(0xffffffffu, bs, 8);
+    bs += __shfl_xor_sync(0xffffffffu, bs, 16);
+    if (lane < nh) lm1[b] = bm + __logf(bs);
+    dmax = fmaxf(dmax, r.delta);
+    const float m_new = fmaxf(m_run, bm);
+    const float alpha = fast_exp(m_run - m_new);
+    const float beta = fast_exp(bm - m_new);
+    l_run = l_run * alpha + bs * beta;
+    m_run = m_new;
+    S.pbuf[warp][t0][h] = e0 * beta;
+    S.pbuf[warp][t1][h] = e1 * beta;
+    if (lane < H) S.abuf[warp][lane] = alpha;
+    __syncwarp();
+
+    // ---- speculative phase 2: INT4 values, lane owns channels 4l..4l+3 --------
+    const float4 al = *reinterpret_cast<const float4*>(S.abuf[warp]);
+    const float alv[4] = {al.x, al.y, al.z, al.w};
+#pragma unroll
+    for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[hh][j] *= alv[hh];
+    const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+    const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+    const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const uint4* vm = reinterpret_cast<const uint4*>(rec + OFF_VMETA + g * 64);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const uint4 mm = vm[q4];
+      const uint32_t mv[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int t = q4 * 4 + k;
+        const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
+        const __half2 so = *reinterpret_cast<const __half2*>(&mv[k]);
+        const float2 sof = __half22float2(so);
+        const float s16 = 16.f * sof.x;
+        const float op = fmaf(-16.f, sof.x, sof.y);
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t bits = ((cw << (19 - 4 * j)) & 0x00780000u) | 0x3F800000u;
+          v[j] = fmaf(__uint_as_float(bits), s16, op);
+        }
+        const float4 p4 = *reinterpret_cast<const float4*>(S.pbuf[warp][t]);
+        const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+        for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[hh][j] = fmaf(pv[hh], v[j], o[hh][j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && i + PA_STAGES < nmine) {
+      fence_proxy_async();
+      mbar_expect_tx(&S.bar[warp][s], REC);
+      bulk_g2s(S.stage[warp][s], ubase + (size_t)(b + PA_WARPS * PA_STAGES) * REC, REC,
+               &S.bar[warp][s]);
+    }
+  }
+
+  // ---- merge the four warps of the CTA, write the split state ---------------
+  __syncthreads();
+  float* mw = reinterpret_cast<float*>(S.stage);        // [warp][h][4]: m, l, dmax
+  float* ow = mw + PA_WARPS * H * 4;                     // [warp][h][D]
+  if (lane < H) {
+    mw[(warp * H + lane) * 4 + 0] = m_run;
+    mw[(warp * H + lane) * 4 + 1] = l_run;
+    mw[(warp * H + lane) * 4 + 2] = dmax;
+  }
+#pragma unroll
+  for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) ow[(warp * H + hh) * D + lane * 4 + j] = o[hh][j];
+  __syncthreads();
+  const int ch = tid;  // 128 threads = 128 channels
+  for (int hh = 0; hh < H; ++hh) {
+    float M = ninf(), dm = 0.f;
+    for (int w = 0; w < PA_WARPS; ++w) {
+      M = fmaxf(M, mw[(w * H + hh) * 4 + 0]);
+      dm = fmaxf(dm, mw[(w * H + hh) * 4 + 2]);
+    }
+    float L = 0.f, O = 0.f;
+    if (M != ninf()) {
+      for (int w = 0; w < PA_WARPS; ++w) {
+        const float mwv = mw[(w * H + hh) * 4 + 0];
+        if (mwv == ninf()) continue;
+        const float sc = fast_exp(mwv - M);
+        L += mw[(w * H + hh) * 4 + 1] * sc;
+        O += ow[(w * H + hh) * D + ch] * sc;
+      }
+    }
+    float* outp = st.split_state + (((size_t)u * st.n_splits + sp) * H + hh) * CKV_SPLIT_FLOATS;
+    if (ch == 0) {
+      outp[0] = M;
+      outp[1] = L;
+      outp[2] = dm;
+      outp[3] = 0.f;
+    }
+    outp[4 + ch] = O;
+  }
+}
+
+// =============================================================================
+// select
+// =============================================================================
+constexpr int SEL_THREADS = 512;
+constexpr int SEL_MAXSORT = 1024;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
+  // 512 threads; returns exclusive prefix of v, writes the block total
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < SEL_THREADS / 32) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < SEL_THREADS / 32) wsum[lane] = w;
+    if (lane == SEL_THREADS / 32 - 1) *total = w;
+  }
+  __syncthreads();
+  int before = (warp > 0) ? wsum[warp - 1] : 0;
+  int r = before + x - v;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum_d(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < SEL_THREADS / 32; ++w) t += red[w];
+    red[SEL_THREADS / 32] = t;
+  }
+  __syncthreads();
+  t = red[SEL_THREADS / 32];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ float block_max_f(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = red[0];
+    for (int w = 1; w < SEL_THREADS / 32; ++w) t = fmaxf(t, red[w]);
+    red[SEL_THREADS / 32] = t;
+  }
+  __syncthreads();
+  float t = red[SEL_THREADS / 32];
+  __syncthreads();
+  return t;
+}
+
+struct SelSmem {
+  unsigned long long sortk[SEL_MAXSORT];
+  double cum[SEL_MAXSORT];
+  float qv[D];
+  float ps[B];
+  int hist[256];
+  int wsum[32];
+  int misc[16];
+  double redd[40];
+  float redf[40];
+};
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
+  uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const ckv_policy& pol = a.pol;
+  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nh = st.n_heads;
+  const int nb = c.n_blocks[u];
+  const int pl = c.partial_len[u];
+  const size_t hu = (size_t)u * nh + h;
+  const float* lm = st.lm1 + hu * c.max_blocks;
+  HeadState& hs = *reinterpret_cast<HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+
+  if (tid < D) S.qv[tid] = (float)(st.q[hu * D + tid] * 0.08838834764831845);
+  for (int i = tid; i < (c.max_blocks + 31) / 32; i += SEL_THREADS) fmask[i] = 0u;
+  __syncthreads();
+
+  // ---- partial block on originals (attention.py:98-104) ------------------------
+  if (warp < pl) {
+    const uint16_t* pk = c.partial_k + ((size_t)u * B + warp) * D;
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      acc = fmaf(__half2float(__ushort_as_half(pk[lane * 4 + j])), S.qv[lane * 4 + j], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) S.ps[warp] = acc;
+  }
+  __syncthreads();
+  float mp = ninf(), lp = 0.f;
+  for (int t = 0; t < pl; ++t) mp = fmaxf(mp, S.ps[t]);
+  for (int t = 0; t < pl; ++t) lp += expf(S.ps[t] - mp);
+  const float lmp = (pl > 0) ? mp + logf(lp) : ninf();
+  if (tid < D) {
+    float acc = 0.f;
+    for (int t = 0; t < pl; ++t)
+      acc = fmaf(expf(S.ps[t] - mp),
+                 __half2float(__ushort_as_half(c.partial_v[((size_t)u * B + t) * D + tid])), acc);
+    hs.np_[tid] = acc;
+  }
+
+  // ---- merge the pass-A splits ---------------------------------------------------
+  const int nsp = (nb + st.blocks_per_split - 1) / st.blocks_per_split;
+  {
+    float M = ninf(), dm = 0.f;
+    for (int s = 0; s < nsp; ++s) {
+      const float* sp = st.split_state + (((size_t)u * st.n_splits + s) * H + h) * CKV_SPLIT_FLOATS;
+      M = fmaxf(M, sp[0]);
+      dm = fmaxf(dm, sp[2]);
+    }
+    float L = 0.f, O = 0.f;
+    if (M != ninf()) {
+      for (int s = 0; s < nsp; ++s) {
+        const float* sp = st.split_state + (((size_t)u * st.n_splits + s) * H + h) * CKV_SPLIT_FLOATS;
+        if (sp[0] == ninf()) continue;
+        const float sc = expf(sp[0] - M);
+        L += sp[1] * sc;
+        if (tid < D) O += sp[4 + tid] * sc;
+      }
+    }
+    if (tid < D) hs.oA[tid] = O;
+    if (tid == 0) {
+      hs.mA = M;
+      hs.lA = L;
+      hs.delta = dm;
+      hs.mp = mp;
+      hs.lp = lp;
+    }
+  }
+
+  // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
+  float lmax = lmp;
+  for (int b = tid; b < nb; b += SEL_THREADS) lmax = fmaxf(lmax, lm[b]);
+  lmax = block_max_f(lmax, S.redf);
+  double se = 0.0;
+  for (int b = tid; b < nb; b += SEL_THREADS) se += exp((double)lm[b] - (double)lmax);
+  if (tid == 0 && pl > 0) se += exp((double)lmp - (double)lmax);
+  se = block_sum_d(se, S.redd);
+  const double lse = (double)lmax + log(se);
+  const double pmass = (pl > 0) ? exp((double)lmp - lse) : 0.0;
+
+  // ---- radix select of the top K_sel blocks by l' (ties -> lower index) -----------
+  const int kwant = (pol.rung1_enabled ? 2 * pol.k_max : pol.k_max) + 1;
+  const int ksel = min(nb, min(kwant, SEL_MAXSORT));
+  int n_sorted = 0;
+  if (ksel > 0) {
+    uint32_t prefix = 0u, mask = 0u;
+    int remaining = ksel;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += SEL_THREADS) S.hist[i] = 0;
+      __syncthreads();
+      for (int b = tid; b < nb; b += SEL_THREADS) {
+        const uint32_t k = okey(lm[b]);
+        if ((k & mask) == prefix) atomicAdd(&S.hist[(k >> shift) & 255u], 1);
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // lane owns digits 255-8*lane .. 248-8*lane (descending)
+        int cnt[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          cnt[j] = S.hist[255 - 8 * lane - j];
+          tot += cnt[j];
+        }
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        int above = incl - tot;  // count in digits strictly greater than this lane's range
+        int found = -1, above_d = 0;
+        for (int j = 0; j < 8; ++j) {
+          if (found < 0 && above + cnt[j] >= remaining) {
+            found = 255 - 8 * lane - j;
+            above_d = above;
+          }
+          above += cnt[j];
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
+        const int src = __ffs(bal) - 1;
+        const int dig = __shfl_sync(0xffffffffu, found, src);
+        const int abv = __shfl_sync(0xffffffffu, above_d, src);
+        if (lane == 0) {
+          S.misc[0] = dig;
+          S.misc[1] = abv;
+        }
+      }
+      __syncthreads();
+      prefix |= (uint32_t)S.misc[0] << shift;
+      mask |= 255u << shift;
+      remaining -= S.misc[1];
+      __syncthreads();
+    }
+    // prefix = threshold key T; take all keys > T and the first `remaining` == T
+    const int per = (nb + SEL_THREADS - 1) / SEL_THREADS;
+    const int lo_i = tid * per, hi_i = min(nb, lo_i + per);
+    int ngt = 0, neq = 0;
+    for (int b = lo_i; b < hi_i; ++b) {
+      const uint32_t k = okey(lm[b]);
+      ngt += (k > prefix);
+      neq += (k == prefix);
+    }
+    int tot_gt, tot_eq;
+    const int off_gt = block_excl_scan(ngt, S.wsum, &S.misc[2]);
+    tot_gt = S.misc[2];
+    const int off_eq = block_excl_scan(neq, S.wsum, &S.misc[3]);
+    tot_eq = S.misc[3];
+    (void)tot_eq;
+    int pg = off_gt, pe = off_eq;
+    for (int b = lo_i; b < hi_i; ++b) {
+      const uint32_t k = okey(lm[b]);
+      const unsigned long long comp =
+          ((unsigned long long)k << 32) | (unsigned long long)(0xffffffffu - (uint32_t)b);
+      if (k > prefix) {
+        S.sortk[pg++] = comp;
+      } else if (k == prefix) {
+        if (pe < remaining) S.sortk[tot_gt + pe] = comp;
+        ++pe;
+      }
+    }
+    n_sorted = ksel;
+    int P = 1;
+    while (P < n_sorted) P <<= 1;
+    for (int i = n_sorted + tid; i < P; i += SEL_THREADS) S.sortk[i] = 0ull;
+    __syncthreads();
+    // bitonic sort, descending
+    for (int k = 2; k <= P; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < P; i += SEL_THREADS) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const unsigned long long x = S.sortk[i], y = S.sortk[ixj];
+            const bool desc = ((i & k) == 0);
+            if (desc ? (x < y) : (x > y)) {
+              S.sortk[i] = y;
+              S.sortk[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
+  for (int i = tid; i < n_sorted; i += SEL_THREADS) {
+    const uint32_t k = (uint32_t)(S.sortk[i] >> 32);
+    const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    S.cum[i] = exp((double)__uint_as_float(bits) - lse);
+  }
+  __syncthreads();
+  if (warp == 0) {  // sequential-order prefix sum in fp64 (one warp, chunked)
+    double carry = pmass;
+    for (int base = 0; base < n_sorted; base += 32) {
+      const int i = base + lane;
+      double x = (i < n_sorted) ? S.cum[i] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < n_sorted) S.cum[i] = carry + x;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int kcov = -1;
+    for (int i = 0; i < n_sorted; ++i)
+      if (S.cum[i] >= pol.tau_cov) {
+        kcov = i + 1;
+        break;
+      }
+    if (kcov < 0 && n_sorted == nb) kcov = nb;
+    int kstar;
+    if (nb == 0) {
+      kstar = 0;
+      kcov = 0;
+    } else {
+      const int kc_eff = (kcov < 0) ? 0x3fffffff : kcov;
+      kstar = min(max(kc_eff, pol.k_min), min(pol.k_max, nb));
+    }
+    int kp = kstar;
+    if (pol.rung1_enabled) kp = min(2 * kstar, nb);
+    S.misc[4] = kcov;
+    S.misc[5] = kstar;
+    S.misc[6] = kp;
+  }
+  __syncthreads();
+  const int kcov = S.misc[4], kstar = S.misc[5], kp = S.misc[6];
+  int32_t* order = st.order + hu * st.kcap;
+  for (int i = tid; i < kp; i += SEL_THREADS) {
+    const int b = (int)(0xffffffffu - (uint32_t)(S.sortk[i] & 0xffffffffull));
+    order[i] = b;
+    atomicOr(&fmask[b >> 5], 1u << (b & 31));
+  }
+  __syncthreads();
+
+  // ---- tail mass, rung 2, E_val tail, work list (fallback.py:141-161, certifier.py:153-160)
+  const float* eta = c.eta + (size_t)u * c.max_blocks;
+  const bool r2 = pol.rung2_enabled != 0;
+  double at = 0.0, et = 0.0;
+  const int per = (nb + SEL_THREADS - 1) / SEL_THREADS;
+  const int lo_i = tid * per, hi_i = min(nb, lo_i + per);
+  int nv = 0, nvx = 0;
+  for (int b = lo_i; b < hi_i; ++b) {
+    const double pb = exp((double)lm[b] - lse);
+    const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
+    const double pe = pb * (double)eta[b];
+    const bool inV = r2 && (pe > pol.v_tol);
+    if (!inF) at += pb;
+    if (!inF && !inV) et += pe;
+    nv += inV;
+    nvx += (inV && !inF);
+  }
+  at = block_sum_d(at, S.redd);
+  et = block_sum_d(et, S.redd);
+  const int vo = block_excl_scan(nv, S.wsum, &S.misc[7]);
+  const int xo = block_excl_scan(nvx, S.wsum, &S.misc[8]);
+  const int n_v = S.misc[7], n_vx = S.misc[8];
+  {
+    int32_t* vlist = st.vlist + hu * c.max_blocks;
+    int32_t* work = st.work + hu * st.wcap;
+    int pv = vo, px = xo;
+    for (int b = lo_i; b < hi_i; ++b) {
+      const double pb = exp((double)lm[b] - lse);
+      const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
+      const bool inV = r2 && (pb * (double)eta[b] > pol.v_tol);
+      if (inV) vlist[pv++] = b;
+      if (inV && !inF) work[kp + px++] = (b << 2) | 2;
+    }
+    for (int i = tid; i < kp; i += SEL_THREADS) {
+      const int b = order[i];
+      const double pb = exp((double)lm[b] - lse);
+      const bool inV = r2 && (pb * (double)eta[b] > pol.v_tol);
+      work[i] = (b << 2) | 1 | (inV ? 2 : 0);
+    }
+  }
+  if (tid == 0) {
+    st.n_work[hu] = kp + n_vx;
+    hs.lse = lse;
+    hs.alpha_hat = (kp >= nb) ? 0.0 : at;
+    hs.e_tail = et;
+    hs.partial_mass = pmass;
+    float tm = ninf();
+    if (kp < nb && kp < n_sorted) {
+      const uint32_t k = (uint32_t)(S.sortk[kp] >> 32);
+      const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+      tm = __uint_as_float(bits);
+    }
+    hs.tailmax = tm;
+    hs.kprime = kp;
+    hs.kstar0 = kstar;
+    hs.n_v = n_v;
+    hs.k_cov = kcov;
+    ckv_cert& ct = st.cert[hu];
+    ct.partial_mass = pmass;
+    ct.k_star = kp;
+    ct.k_star0 = kstar;
+    ct.k_coverage = kcov;
+    ct.n_value_promoted = n_v;
+    uint32_t fl = CKV_F_ACTIVE;
+    if (pol.rung1_enabled && kp != kstar) fl |= CKV_F_RUNG1;
+    if (n_v > 0) fl |= CKV_F_RUNG2;
+    if (kcov != kstar) fl |= CKV_F_CLAMPED;
+    ct.flags = fl;
+  }
+}
+
+// =============================================================================
+// pass B
+// =============================================================================
+constexpr int PB_WARPS = 4;
+
+struct PassBSmem {
+  uint8_t rec[PB_WARPS][REC];
+  float qh[H * D];
+  float sq[PB_WARPS][B];
+  float so[PB_WARPS][B];
+  float mrg[PB_WARPS][8];
+  double mrgd[PB_WARPS][2];
+};
+
+__global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const int ck = blockIdx.x, h = blockIdx.y, u = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nh = st.n_heads;
+  const size_t hu = (size_t)u * nh + h;
+  const int nwork = st.n_work[hu];
+  const int C = gridDim.x;
+  const int ipc = st.items_per_chunk;
+  float* cs = st.chunk_state + (hu * C + ck) * CKV_CHUNK_FLOATS;
+  if (ck * ipc >= nwork) {
+    if (tid == 0) cs[0] = ninf();
+    return;
+  }
+  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    int hh = i / D;
+    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
+                        : 0.f;
+  }
+  __syncthreads();
+  QFrag f;
+  load_qfrag(f, S.qh, lane);
+
+  const float* qme = S.qh + h * D;
+  const float* eta = c.eta + (size_t)u * c.max_blocks;
+  const int32_t* work = st.work + hu * st.wcap;
+  float* lm2 = st.lm2 + hu * st.kcap;
+  const double lse = hs.lse;
+  float m_c = hs.mA;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float dden = 0.f, canary = 0.f;
+  double eF = 0.0, sF = 0.0;
+  const int g = lane >> 2;
+  const size_t ub = (size_t)u * c.max_blocks;
+
+  for (int base = ck * ipc; base < nwork; base += C * ipc) {
+    const int end = min(nwork, base + ipc);
+    for (int it = base + warp; it < end; it += PB_WARPS) {
+      const int e = work[it];
+      const int b = e >> 2;
+      const bool inF = e & 1, inV = (e >> 1) & 1;
+      // stage the Tier-1 record
+      const uint4* src = reinterpret_cast<const uint4*>(c.tier1 + (ub + b) * REC);
+      uint4* dst = reinterpret_cast<uint4*>(S.rec[warp]);
+      for (int k = lane; k < REC / 16; k += 32) dst[k] = src[k];
+      __syncwarp();
+      const uint8_t* rec = S.rec[warp];
+      BlockScores r = phase1_block(f, rec, c.kscale_max[ub + b], lane);
+      if ((lane & 3) == h) {
+        S.sq[warp][lane >> 2] = r.s0;
+        S.sq[warp][(lane >> 2) + 8] = r.s1;
+      }
+      if (inF || inV) {
+        if (!c.tier2_valid[ub + b] && lane == 0) atomicOr(&c.status[CKV_ST_TIER2], 1);
+      }
+      if (inF) {  // original-key scores: two lanes per token, 64 channels each
+        const int t = lane >> 1, hf = lane & 1;
+        const uint4* kp = reinterpret_cast<const uint4*>(c.tier2_k + ((ub + b) * B + t) * D + hf * 64);
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint4 w = kp[k];
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&ww[j]));
+            s = fmaf(kf.x, qme[hf * 64 + k * 8 + 2 * j], s);
+            s = fmaf(kf.y, qme[hf * 64 + k * 8 + 2 * j + 1], s);
+          }
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (hf == 0) S.so[warp][t] = s;
+      }
+      __syncwarp();
+      float sn[B], sq[B];
+      float mx = ninf();
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        sq[t] = S.sq[warp][t];
+        sn[t] = inF ? S.so[warp][t] : sq[t];
+        mx = fmaxf(mx, sn[t]);
+      }
+      const float m_new = fmaxf(m_c, mx);
+      const float resc = fast_exp(m_c - m_new);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] *= resc;
+      dden *= resc;
+      m_c = m_new;
+      if (inF) {
+        float bm = ninf(), gap = 0.f;
+#pragma unroll
+        for (int t = 0; t < B; ++t) {
+          bm = fmaxf(bm, sn[t]);
+          gap = fmaxf(gap, fabsf(sn[t] - sq[t]));
+        }
+        float bsum = 0.f;
+#pragma unroll
+        for (int t = 0; t < B; ++t) bsum += expf(sn[t] - bm);
+        const float lb = bm + logf(bsum);
+        canary = fmaxf(canary, gap);
+        if (lane == 0) lm2[it] = lb;
+        const double rb = exp((double)lb - lse);
+        sF += rb;
+        if (!inV) eF += rb * (double)eta[b];
+      }
+      // values: lane owns channels 4*lane .. 4*lane+3
+      const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+      const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const uint32_t* vm = reinterpret_cast<const uint32_t*>(rec + OFF_VMETA + g * 64);
+      const uint16_t* vorig = c.tier2_v + (ub + b) * B * D + lane * 4;
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
+        const uint32_t mm = vm[t];
+        const float2 sof = __half22float2(*reinterpret_cast<const __half2*>(&mm));
+        const float s16 = 16.f * sof.x;
+        const float op = fmaf(-16.f, sof.x, sof.y);
+        float vq[4], vn[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t bits = ((cw << (19 - 4 * j)) & 0x00780000u) | 0x3F800000u;
+          vq[j] = fmaf(__uint_as_float(bits), s16, op);
+          vn[j] = vq[j];
+        }
+        if (inV) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
+          const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+          const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+          vn[0] = a0.x;
+          vn[1] = a0.y;
+          vn[2] = a1.x;
+          vn[3] = a1.y;
+        }
+        const float wq = expf(sq[t] - m_c);
+        if (inF) {
+          const float wn = expf(sn[t] - m_c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] += wn * vn[j] - wq * vq[j];
+          dden += wn - wq;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] = fmaf(wq, vn[j] - vq[j], acc[j]);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  // ---- merge warps -------------------------------------------------------------------
+  if (lane == 0) {
+    S.mrg[warp][0] = m_c;
+    S.mrg[warp][1] = dden;
+    S.mrg[warp][2] = canary;
+    S.mrgd[warp][0] = eF;
+    S.mrgd[warp][1] = sF;
+  }
+  __syncthreads();
+  float* accs = reinterpret_cast<float*>(S.rec);  // [warp][D]
+#pragma unroll
+  for (int j = 0; j < 4; ++j) accs[warp * D + lane * 4 + j] = acc[j];
+  __syncthreads();
+  float M = ninf();
+  for (int w = 0; w < PB_WARPS; ++w) M = fmaxf(M, S.mrg[w][0]);
+  float O = 0.f, DD = 0.f;
+  for (int w = 0; w < PB_WARPS; ++w) {
+    const float sc = (S.mrg[w][0] == ninf()) ? 0.f : expf(S.mrg[w][0] - M);
+    O += accs[w * D + tid] * sc;
+    DD += S.mrg[w][1] * sc;
+  }
+  cs[8 + tid] = O;
+  if (tid == 0) {
+    float cn = 0.f;
+    double e2 = 0.0, s2 = 0.0;
+    for (int w = 0; w < PB_WARPS; ++w) {
+      cn = fmaxf(cn, S.mrg[w][2]);
+      e2 += S.mrgd[w][0];
+      s2 += S.mrgd[w][1];
+    }
+    cs[0] = M;
+    cs[1] = DD;
+    cs[2] = cn;
+    cs[3] = 0.f;
+    reinterpret_cast<double*>(cs + 4)[0] = e2;
+    reinterpret_cast<double*>(cs + 4)[1] = s2;
+  }
+}
+
+// =============================================================================
+// combine
+// =============================================================================
+__global__ void __launch_bounds__(128) k_combine(StepArgs a) {
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const ckv_policy& pol = a.pol;
+  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+  const int nh = st.n_heads;
+  const size_t hu = (size_t)u * nh + h;
+  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+  const int C = st.n_chunks;
+  const float* cs0 = st.chunk_state + hu * C * CKV_CHUNK_FLOATS;
+  const int pl = c.partial_len[u];
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+
+  float M = (hs.lA > 0.f) ? hs.mA : ninf();
+  for (int k = 0; k < C; ++k) M = fmaxf(M, cs0[k * CKV_CHUNK_FLOATS]);
+  if (pl > 0) M = fmaxf(M, hs.mp);
+  float den = 0.f, num = 0.f;
+  if (hs.lA > 0.f) {
+    const float sc = expf(hs.mA - M);
+    den += hs.lA * sc;
+    num += hs.oA[tid] * sc;
+  }
+  float canary = 0.f;
+  double eF = 0.0, sF = 0.0;
+  for (int k = 0; k < C; ++k) {
+    const float* cs = cs0 + k * CKV_CHUNK_FLOATS;
+    if (cs[0] == ninf()) continue;
+    const float sc = expf(cs[0] - M);
+    den += cs[1] * sc;
+    num += cs[8 + tid] * sc;
+    canary = fmaxf(canary, cs[2]);
+    eF += reinterpret_cast<const double*>(cs + 4)[0];
+    sF += reinterpret_cast<const double*>(cs + 4)[1];
+  }
+  if (pl > 0) {
+    const float sc = expf(hs.mp - M);
+    den += hs.lp * sc;
+    num += hs.np_[tid] * sc;
+  }
+  const float out = num / den;
+  if (!isfinite(out) || !(den > 0.f)) atomicOr(&bad, 1);
+  st.out[hu * D + tid] = out;
+  __syncthreads();
+
+  if (tid == 0) {
+    ckv_cert& ct = st.cert[hu];
+    uint32_t fl = ct.flags;
+    const int kp = hs.kprime;
+    const int r = pol.ranking_depth;
+    const int32_t* order = st.order + hu * st.kcap;
+    const float* lm2 = st.lm2 + hu * st.kcap;
+    const double delta = (double)hs.delta;
+    if (pol.ranking_checks_enabled && kp > 0) {
+      if (kp < r) {
+        fl |= CKV_F_RANKING;
+      } else {
+        // top-r of the phase-2 log-masses (ties -> lower block index) vs the
+        // phase-1 order prefix (fallback.py:164-187, harness.py:231-250)
+        int picked[64];
+        float rth = 0.f;
+        bool same = true;
+        const int rr = min(r, 64);
+        for (int j = 0; j < rr; ++j) {
+          int best = -1;
+          float bv = 0.f;
+          int bb = 0x7fffffff;
+          for (int i = 0; i < kp; ++i) {
+            bool used = false;
+            for (int q = 0; q < j; ++q) used |= (picked[q] == i);
+            if (used) continue;
+            const float v = lm2[i];
+            const int bi = order[i];
+            if (best < 0 || v > bv || (v == bv && bi < bb)) {
+              best = i;
+              bv = v;
+              bb = bi;
+            }
+          }
+          picked[j] = best;
+          rth = bv;
+          if (order[j] != bb) same = false;
+        }
+        if (!same) fl |= CKV_F_RANKING;
+        if (hs.tailmax != ninf() && !((double)hs.tailmax + delta <= (double)rth)) fl |= CKV_F_BOUNDARY;
+      }
+    }
+    if (pol.canary_enabled && kp > 0) {
+      if (!((double)canary <= delta + pol.epsilon_guard)) fl |= CKV_F_CANARY;
+    }
+    if (bad) fl |= CKV_F_NUMERIC;
+    const double vmax = (double)c.v_max[u];
+    const double at = hs.alpha_hat;
+    const double denomE = at + hs.partial_mass + sF;
+    ct.delta_h = delta;
+    ct.est_tail_mass = at;
+    ct.v_max = vmax;
+    ct.e_key_tight = 2.0 * vmax * exp(2.0 * delta) * at * (exp(2.0 * delta) - 1.0);
+    // certifier.py:191-212 records both exponent modes; returned_e_key uses mode 3
+    ct.e_key_impl = 2.0 * vmax * exp(3.0 * delta) * at * (exp(2.0 * delta) - 1.0);
+    ct.e_val = (denomE > 0.0) ? (hs.e_tail + eF) / denomE : 0.0;
+    ct.canary_gap = (double)canary;
+    ct.flags = fl;
+    int kind = 0;
+    if (fl & (CKV_F_CANARY | CKV_F_NUMERIC)) kind = 2;
+    else if (fl & (CKV_F_RANKING | CKV_F_BOUNDARY)) kind = 1;
+    ct.returned_kind = kind;
+  }
+}
+
+// =============================================================================
+// kernel-backend plugin (pure.py:16-66) -- parity surface, not the hot path
+// =============================================================================
+__global__ void k_block_logmass(const double* s, const int64_t* bnd, int nb, double* bmax,
+                                double* bsum, double* lmass) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nb) return;
+  const int64_t lo = bnd[i], hi = bnd[i + 1];
+  double m = -INFINITY;
+  for (int64_t t = lo; t < hi; ++t) m = fmax(m, s[t]);
+  double acc = 0.0;
+  for (int64_t t = lo; t < hi; ++t) acc += exp(s[t] - m);
+  bmax[i] = m;
+  bsum[i] = acc;
+  lmass[i] = m + log(acc);
+}
+
+__global__ void k_fused_attend(const float* s, const float* v, const int64_t* bnd, int nb, int d,
+                               float* out, float* ml) {
+  float m = -INFINITY, l = 0.f;
+  const int ch = threadIdx.x;
+  float o = 0.f;
+  for (int i = 0; i < nb; ++i) {
+    const int64_t lo = bnd[i], hi = bnd[i + 1];
+    float mn = m;
+    for (int64_t t = lo; t < hi; ++t) mn = fmaxf(mn, s[t]);
+    const float sc = expf(m - mn);
+    float w = 0.f;
+    o *= sc;
+    for (int64_t t = lo; t < hi; ++t) {
+      const float p = expf(s[t] - mn);
+      w += p;
+      if (ch < d) o = fmaf(p, v[t * d + ch], o);
+    }
+    l = l * sc + w;
+    m = mn;
+  }
+  if (ch < d) out[ch] = o / l;
+  if (ch == 0) {
+    ml[0] = m;
+    ml[1] = l;
+  }
+}
+
+// =============================================================================
+// launchers
+// =============================================================================
+extern int g_launches;
+
+cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                          int host_max_blocks, cudaStream_t s) {
+  g_launches = 0;
+  StepArgs a{*c, *st, *pol};
+  const size_t smA = sizeof(PassASmem);
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(PassBSmem));
+    attrs = true;
+  }
+  const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
+  if (nsplit_used > 0) {
+    k_pass_a<<<dim3(nsplit_used, c->n_units), PA_WARPS * 32, smA, s>>>(a);
+    ++g_launches;
+  }
+  const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
+  k_select<<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+  ++g_launches;
+  k_pass_b<<<dim3(st->n_chunks, st->n_heads, c->n_units), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  ++g_launches;
+  k_combine<<<dim3(st->n_heads, c->n_units), 128, 0, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_logmass(const double* sc, const int64_t* bnd, int nb, double* bm,
+                                 double* bs, double* lm, cudaStream_t s) {
+  if (nb <= 0) return cudaSuccess;
+  k_block_logmass<<<(nb + 127) / 128, 128, 0, s>>>(sc, bnd, nb, bm, bs, lm);
+  return cudaGetLastError();
+}
+cudaError_t launch_fused_attend(const float* sc, const float* v, const int64_t* bnd, int nb, int d,
+                                float* out, float* ml, cudaStream_t s) {
+  int th = ((d + 31) / 32) * 32;
+  if (th < 32) th = 32;
+  k_fused_attend<<<1, th, 0, s>>>(sc, v, bnd, nb, d, out, ml);
+  return cudaGetLastError();
+}
+
+}  // namespace ckv

@@ -1,0 +1,133 @@
+// Phase-1 block scoring on the tensor cores, shared by pass A and pass B so
+// both see bit-identical quantized scores.
+//
+// s'_t,h = sum_c q'_hc (code_tc * sigma_c + z_c),  q' = q / sqrt(d)
+//        = 2^(eQ_h + eS_b - 21) * sum_c code_tc * X_hc + constz_h
+// with X_hc = rint(q'_hc 2^(21-eQ_h) * sigma_c 2^(-eS_b)), |X| < 2^21.
+// The INT8 codes are the A operand of mma.m16n8k32.s8.u8 straight from the
+// record (no conversion); X is fed as three unsigned bytes of U = X + 2^22
+// (taken directly from the fp32 bit pattern of fma(x, 1, 1.5*2^23)), and a
+// column of ones recovers sum_c code_tc to remove the 2^22 bias.
+//
+// B-operand column map (n = lane/4 for the fragment that a lane supplies):
+//   tile 0: n = 2h + {0,1}  -> head h, byte 0 / byte 1 of U
+//   tile 1: n = 2h          -> head h, byte 2 of U;  n = 2h + 1 -> ones
+// so accumulator lane l ends up owning head h = l % 4 for tokens l/4, l/4+8.
+#pragma once
+#include "common.cuh"
+
+namespace ckv {
+
+struct QFrag {
+  float qsc[32];   // q'_{h,c} * 2^(21-eQ_h) for h = lane/8, the lane's 32 channels
+  float aw[32];    // odd (lane/4): qsc (for sum q' z); even: |qsc| (for Delta)
+  int eq_l;        // exponent of head lane%4: max|q'_h| < 2^eq_l
+};
+
+// channel of the lane's j-th B element in k-tile kt
+__device__ __forceinline__ int bchan(int lane, int kt, int j) {
+  return kt * 32 + (lane & 3) * 4 + (j & 3) + ((j >> 2) << 4);
+}
+
+__device__ __forceinline__ float pow2f(int e) {  // exact 2^e for e in [-126, 127]
+  return __uint_as_float((uint32_t)(e + 127) << 23);
+}
+
+// qh: q'[4][128] float in shared memory.
+__device__ inline void load_qfrag(QFrag& f, const float* qh, int lane) {
+  const int hb = lane >> 3;
+  int eq_b = 0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    float m = 0.f;
+    for (int c = lane; c < D; c += 32) m = fmaxf(m, fabsf(qh[h * D + c]));
+    m = warp_max(m);
+    const int e = (m > 0.f) ? (ilogbf(m) + 1) : 0;
+    if (h == (lane & 3)) f.eq_l = e;
+    if (h == hb) eq_b = e;
+  }
+  const float sc = ldexpf(1.0f, 21 - eq_b);
+  const bool odd = (lane >> 2) & 1;
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = qh[hb * D + bchan(lane, kt, j)] * sc;
+      f.qsc[kt * 8 + j] = v;
+      f.aw[kt * 8 + j] = odd ? v : fabsf(v);
+    }
+  }
+}
+
+struct BlockScores {
+  float s0, s1;    // scores of tokens lane/4 and lane/4+8 for head lane%4
+  float delta;     // Delta_b for head lane%4 (already / 2 / sqrt(d) folded)
+};
+
+// rec: Tier-1 record in shared (or global) memory; smax: the block's max key scale.
+__device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_t* rec, float smax,
+                                                    int lane) {
+  const float* sig = reinterpret_cast<const float*>(rec + OFF_KSCALE);
+  const float* zz = reinterpret_cast<const float*>(rec + OFF_KOFF);
+  const bool odd = (lane >> 2) & 1;
+  const float* aux = odd ? zz : sig;  // per-lane operand for the Delta / constz sums
+  const int es = ilogbf(smax) + 1;    // smax < 2^es
+  const float sdown = ldexpf(1.0f, -es);
+  const uint32_t sel0 = ((lane >> 2) & 1) ? 0x5151u : 0x4040u;  // byte 1 or 0 of y0,y1
+  const float MAGIC = 12582912.0f;  // 1.5 * 2^23
+  int d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
+  float acc = 0.f;
+#pragma unroll
+  for (int kt = 0; kt < 4; ++kt) {
+    const int cb = kt * 32 + (lane & 3) * 4;
+    const float4 sa = *reinterpret_cast<const float4*>(sig + cb);
+    const float4 sb = *reinterpret_cast<const float4*>(sig + cb + 16);
+    const float4 xa = *reinterpret_cast<const float4*>(aux + cb);
+    const float4 xb = *reinterpret_cast<const float4*>(aux + cb + 16);
+    const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
+    const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    uint32_t y[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      y[j] = __float_as_uint(fmaf(f.qsc[kt * 8 + j], sv[j] * sdown, MAGIC));
+      acc = fmaf(f.aw[kt * 8 + j], xv[j], acc);
+    }
+    // tile 0: byte (lane/4)&1 of the four U values, packed into one register
+    uint32_t b00 = __byte_perm(__byte_perm(y[0], y[1], sel0), __byte_perm(y[2], y[3], sel0), 0x5410);
+    uint32_t b01 = __byte_perm(__byte_perm(y[4], y[5], sel0), __byte_perm(y[6], y[7], sel0), 0x5410);
+    // tile 1: byte 2 (even lane/4) or the ones column (odd lane/4)
+    uint32_t b10 = __byte_perm(__byte_perm(y[0], y[1], 0x6262u), __byte_perm(y[2], y[3], 0x6262u), 0x5410);
+    uint32_t b11 = __byte_perm(__byte_perm(y[4], y[5], 0x6262u), __byte_perm(y[6], y[7], 0x6262u), 0x5410);
+    if (odd) {
+      b10 = 0x01010101u;
+      b11 = 0x01010101u;
+    }
+    const uint4 a = *reinterpret_cast<const uint4*>(rec + OFF_KCODES + kt * 512 + lane * 16);
+    mma_s8u8(d0, a, b00, b01);
+    mma_s8u8(d1, a, b10, b11);
+  }
+  // reduce the Delta / constz partials over the 4 lanes sharing lane/4
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  const int h = lane & 3;
+  const float dsum = __shfl_sync(0xffffffffu, acc, h * 8);      // sum |qsc| sigma (head h)
+  const float zsum = __shfl_sync(0xffffffffu, acc, h * 8 + 4);  // sum qsc z (head h)
+  const float inv_q = ldexpf(1.0f, f.eq_l - 21);
+  const float scl = ldexpf(1.0f, f.eq_l + es - 21);
+  const float constz = zsum * inv_q;
+  BlockScores r;
+  {
+    int lo = d0[0] + 256 * d0[1];
+    int hi = d1[0] - 64 * d1[1];
+    r.s0 = fmaf(fmaf((float)hi, 65536.f, (float)lo), scl, constz);
+  }
+  {
+    int lo = d0[2] + 256 * d0[3];
+    int hi = d1[2] - 64 * d1[3];
+    r.s1 = fmaf(fmaf((float)hi, 65536.f, (float)lo), scl, constz);
+  }
+  r.delta = 0.5f * dsum * inv_q;
+  return r;
+}
+
+}  // namespace ckv

@@ -1,0 +1,259 @@
+"""Certified decode step driver (host side of the C ABI) and the reference API.
+
+``CertifiedDecoder.step`` is the batched certified attention call: one C call
+launches pass A / select / pass B / combine (+ the LRU scratch accounting)
+for every (unit, q-head); the host then reads back the certificate array,
+resolves step-wide Rung 4 (harness.py:362-372) and runs the terminal dense
+fallback with ``scaled_dot_product_attention`` over the FP16 Tier-2 originals
+for the flagged heads only.
+
+``run_decode_step`` / ``run_workload`` keep the reference signatures
+(harness.py:186-394) on top of it.
+"""
+
+import ctypes
+import dataclasses
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _lib
+from .cache import DeviceKVCache, ScratchCache, TieredCache, _ptr, _stream
+from .errors import EmptyCacheError, Tier2UnavailableError
+from .policy import (KINDS, RETURNED_DENSE_ALL_HEADS, RETURNED_QUANTIZED, Certificate,
+                     PolicyConfig, RungFlags, events_from_flags)
+
+D, B = _lib.HEAD_DIM, _lib.BLOCK
+
+CERT_DTYPE = np.dtype([("delta_h", "f8"), ("e_key_tight", "f8"), ("e_key_impl", "f8"),
+                       ("e_val", "f8"), ("est_tail_mass", "f8"), ("v_max", "f8"),
+                       ("canary_gap", "f8"), ("partial_mass", "f8"), ("k_star", "i4"),
+                       ("k_star0", "i4"), ("k_coverage", "i4"), ("n_value_promoted", "i4"),
+                       ("flags", "u4"), ("returned_kind", "i4")])
+assert CERT_DTYPE.itemsize == ctypes.sizeof(_lib.CkvCert)
+
+
+@dataclass
+class StepOutput:
+    """Result of one batched certified decode step."""
+    out: torch.Tensor            # [U, nh, 128] float32 (dense rungs applied)
+    cert: np.ndarray             # [U, nh] CERT_DTYPE
+    kinds: np.ndarray            # [U, nh] 0 quantized, 1 dense per head, 2 dense all heads
+    page_stats: np.ndarray | None
+    staging_bytes: int
+    decoder: "CertifiedDecoder" = field(repr=False)
+
+    def promoted(self, u, h):
+        """Promoted block ids of (unit, head) in mass order (the decision)."""
+        kp = int(self.cert[u, h]["k_star"])
+        return self.decoder.order[u, h, :kp].cpu().numpy()
+
+    def value_promotions(self, u, h):
+        nv = int(self.cert[u, h]["n_value_promoted"])
+        return self.decoder.vlist[u, h, :nv].cpu().numpy()
+
+
+class CertifiedDecoder:
+    """Certified decode over every unit of a DeviceKVCache.
+
+    ``rung4_group`` is the number of consecutive units that share a step-wide
+    Rung 4 (a canary trip in any of them makes all their heads dense); the
+    reference's single-layer run makes it every unit (harness.py:362-372).
+    """
+
+    def __init__(self, cache: DeviceKVCache, policy: PolicyConfig, n_heads=4, scratch=None,
+                 rung4_group=None):
+        if not 1 <= n_heads <= _lib.MAX_QHEADS:
+            raise ValueError("device path supports 1..4 query heads per KV head")
+        self.cache, self.policy, self.nh = cache, policy, int(n_heads)
+        self.lib = cache.lib
+        self.pol_c = policy.to_c()
+        st = _lib.CkvStep()
+        _lib.check(self.lib.ckv_plan(cache.n_units, cache.max_blocks, self.nh,
+                                     ctypes.byref(self.pol_c), ctypes.byref(st)), "ckv_plan")
+        U, NB, nh, dev = cache.n_units, cache.max_blocks, self.nh, cache.device
+        self.q = torch.zeros((U, nh, D), dtype=torch.float64, device=dev)
+        self.out = torch.zeros((U, nh, D), dtype=torch.float32, device=dev)
+        self.cert_buf = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+        self.lm1 = torch.zeros((U, nh, NB), dtype=torch.float32, device=dev)
+        self.split_state = torch.zeros((U, st.n_splits, 4, _lib.SPLIT_FLOATS),
+                                       dtype=torch.float32, device=dev)
+        self.order = torch.zeros((U, nh, st.kcap), dtype=torch.int32, device=dev)
+        self.work = torch.zeros((U, nh, st.wcap), dtype=torch.int32, device=dev)
+        self.n_work = torch.zeros((U, nh), dtype=torch.int32, device=dev)
+        self.vlist = torch.zeros((U, nh, NB), dtype=torch.int32, device=dev)
+        self.lm2 = torch.zeros((U, nh, st.kcap), dtype=torch.float32, device=dev)
+        self.head_state = torch.zeros((U, nh, _lib.HEAD_FLOATS), dtype=torch.float32, device=dev)
+        self.chunk_state = torch.zeros((U, nh, st.n_chunks, _lib.CHUNK_FLOATS),
+                                       dtype=torch.float32, device=dev)
+        self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
+        for name, t in (("q", self.q), ("out", self.out), ("cert", self.cert_buf),
+                        ("lm1", self.lm1), ("split_state", self.split_state),
+                        ("order", self.order), ("work", self.work), ("n_work", self.n_work),
+                        ("vlist", self.vlist), ("lm2", self.lm2),
+                        ("head_state", self.head_state), ("chunk_state", self.chunk_state),
+                        ("page_stats", self.page_stats)):
+            setattr(st, name, _ptr(t))
+        self.st = st
+        self.scratch = scratch
+        if scratch is not None:
+            scratch.bind(cache)
+        self.rung4_group = int(rung4_group or U)
+        self.cert_host = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
+
+    # -- the device step -----------------------------------------------------
+    def launch(self, queries=None):
+        """Enqueue the fast path only (no host sync); returns immediately."""
+        if queries is not None:
+            self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
+        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
+        code = self.lib.ckv_decode_step(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
+                                        ctypes.byref(self.st), sc, self.cache.num_blocks,
+                                        _stream(self.cache.device))
+        _lib.check(code, "ckv_decode_step")
+
+    def step(self, queries, dense=True):
+        """Certified attention for all units: queries [U, nh, 128] (float64)."""
+        if self.cache.num_tokens == 0:
+            raise EmptyCacheError("cannot attend over an empty cache")
+        if self.policy.exploration_rate > 0:
+            raise NotImplementedError(
+                "exploration spot checks are not on the device path yet; use exploration_rate=0")
+        self.launch(queries)
+        self.cert_host.copy_(self.cert_buf, non_blocking=True)
+        torch.cuda.current_stream(self.cache.device).synchronize()
+        st = self.cache.status.cpu()
+        if st[_lib.ST_TIER2]:
+            self.cache.status[_lib.ST_TIER2] = 0
+            raise Tier2UnavailableError("full-precision originals of a promoted block are unavailable")
+        cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh).copy()
+        kinds = cert["returned_kind"].copy()
+        U, g = self.cache.n_units, self.rung4_group
+        r4 = (kinds == 2).any(axis=1)
+        staging = 0
+        for g0 in range(0, U, g):
+            if r4[g0:g0 + g].any():
+                kinds[g0:g0 + g, :] = 2
+                staging += sum(2 * self.cache.num_tokens * D * 2 for _ in range(min(g, U - g0)))
+        if dense:
+            self.dense_fallback(kinds)
+        ps = self.page_stats.cpu().numpy().copy() if self.scratch is not None else None
+        return StepOutput(self.out, cert, kinds, ps, staging, self)
+
+    def dense_fallback(self, kinds):
+        """Rung 3/4: exact attention over the FP16 originals (attention.py:327-342)
+        with scaled_dot_product_attention, for flagged units only."""
+        units = np.nonzero((kinds != 0).any(axis=1))[0]
+        for u in units:
+            u = int(u)
+            self.cache.check_tier2(u)
+            k, v = self.cache.tier2_rows(u)
+            heads = np.nonzero(kinds[u] != 0)[0]
+            q = self.q[u, torch.as_tensor(heads, device=self.q.device)].float()
+            o = F.scaled_dot_product_attention(
+                q[None, :, None, :], k.float()[None, None].expand(1, len(heads), -1, -1),
+                v.float()[None, None].expand(1, len(heads), -1, -1))
+            self.out[u, torch.as_tensor(heads, device=self.q.device)] = o[0, :, 0, :]
+
+
+# -- reference-shaped per-head API --------------------------------------------
+
+
+@dataclass
+class SelectionView:
+    promoted: frozenset
+    k_star: int
+    est_tail_mass: float
+    clamped: bool
+    k_coverage: int
+    partial_mass: float
+    order: np.ndarray
+
+
+@dataclass
+class HeadStepResult:
+    """Same fields as harness.HeadStepResult (harness.py:166-178)."""
+    output: np.ndarray
+    certificate: Certificate
+    events: list
+    page_reports: dict
+    decision: SelectionView
+    value_promotions: frozenset
+    attend: object
+    delta_h: float
+    rung4_requested: bool = False
+
+
+def certificate_from_row(row, head, step, kind=None):
+    fl = int(row["flags"])
+    kind = int(row["returned_kind"]) if kind is None else int(kind)
+    return Certificate(
+        head=int(head), step=int(step), delta_h=float(row["delta_h"]),
+        e_key_tight=float(row["e_key_tight"]), e_key_impl=float(row["e_key_impl"]),
+        e_val=float(row["e_val"]), est_tail_mass=float(row["est_tail_mass"]),
+        v_max=float(row["v_max"]), k_star=int(row["k_star"]), returned_kind=KINDS[kind],
+        rung_flags=RungFlags(rung1=bool(fl & _lib.F_RUNG1), rung2=bool(fl & _lib.F_RUNG2),
+                             rung3=bool(fl & (_lib.F_RANKING | _lib.F_BOUNDARY)),
+                             rung4=bool(fl & (_lib.F_CANARY | _lib.F_NUMERIC))))
+
+
+def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, rng=None,
+                    head=0, step=0):
+    """One q-head through the certified pipeline (harness.py:186-300)."""
+    if not isinstance(cache, TieredCache):
+        raise TypeError("run_decode_step expects a paper_2605_20868_b200.TieredCache")
+    if policy.exploration_rate > 0 and rng is not None:
+        raise NotImplementedError("exploration spot checks are not on the device path yet")
+    q = np.asarray(query, dtype=np.float64).reshape(-1)
+    if q.shape[0] != cache.head_dim:
+        raise ValueError(f"query has length {q.shape[0]}, expected {cache.head_dim}")
+    scratch = None
+    if key_scratch is not None or value_scratch is not None:
+        kc = key_scratch.capacity if key_scratch is not None else 1 << 30
+        vc = value_scratch.capacity if value_scratch is not None else 1 << 30
+        key = ("scr", id(key_scratch), id(value_scratch))
+        scratch = cache.__dict__.setdefault(key, ScratchCache(kc, vc))
+    dkey = ("dec", policy, id(scratch))
+    dec = cache.__dict__.get(dkey)
+    if dec is None:
+        dec = CertifiedDecoder(cache.dev, dataclasses.replace(policy, exploration_rate=0.0),
+                               n_heads=1, scratch=scratch)
+        cache.__dict__[dkey] = dec
+    before = scratch.counters.sum(0).cpu().tolist() if scratch is not None else None
+    res = dec.step(torch.from_numpy(q).reshape(1, 1, D).to(cache.dev.device))
+    row = res.cert[0, 0]
+    kind = int(res.kinds[0, 0])
+    cert = certificate_from_row(row, head, step, kind)
+    reports = {}
+    if scratch is not None:
+        after = scratch.counters.sum(0).cpu().tolist()
+        d = [a - b for a, b in zip(after, before)]
+        if key_scratch is not None:
+            reports["keys"] = {"hits": d[0], "misses": d[1], "bytes": d[2]}
+        if value_scratch is not None:
+            reports["values"] = {"hits": d[3], "misses": d[4], "bytes": d[5]}
+    prom = res.promoted(0, 0)
+    vprom = frozenset(int(b) for b in res.value_promotions(0, 0))
+    decision = SelectionView(frozenset(int(b) for b in prom), int(row["k_star"]),
+                             float(row["est_tail_mass"]),
+                             bool(int(row["flags"]) & _lib.F_CLAMPED), int(row["k_coverage"]),
+                             float(row["partial_mass"]), prom)
+    out = res.out[0, 0].double().cpu().numpy()
+    return HeadStepResult(out, cert, events_from_flags(int(row["flags"]), head, step), reports,
+                          decision, vprom, None, float(row["delta_h"]),
+                          rung4_requested=bool(int(row["flags"]) & (_lib.F_CANARY | _lib.F_NUMERIC)))
+
+
+def dense_attention(query, cache):
+    """Exact attention over the originals of a TieredCache (attention.py:327-342)."""
+    dev = cache.dev
+    if dev.num_tokens == 0:
+        raise EmptyCacheError("cannot attend over an empty cache")
+    dev.check_tier2(0)
+    k, v = dev.tier2_rows(0)
+    q = torch.as_tensor(np.asarray(query, dtype=np.float64)).to(dev.device)
+    s = (k.double() @ q) / np.sqrt(D)
+    w = torch.softmax(s, 0)
+    return (w @ v.double()).cpu().numpy()

@@ -1,0 +1,90 @@
+"""Host-side logic of the drop-in API (no GPU): policy validation, event
+decoding, certificate views, storage accounting and the telemetry schema,
+checked against the oracle restatement."""
+
+import numpy as np
+import pytest
+
+from paper_2605_20868_b200 import _lib
+from paper_2605_20868_b200.harness import aggregate_telemetry, step_record, WorkloadConfig, synth_arrays
+from paper_2605_20868_b200.policy import (Certificate, FallbackEvent, PolicyConfig, RungFlags,
+                                          events_from_flags)
+from paper_2605_20868_b200.cache import storage_table
+
+import oracle
+from oracle.step import aggregate as oracle_aggregate, make_workload
+
+
+def test_policy_validation_matches_reference():
+    with pytest.raises(ValueError, match="tau_cov"):
+        PolicyConfig(tau_cov=1.5)
+    with pytest.raises(ValueError, match="k_min"):
+        PolicyConfig(k_min=5, k_max=2)
+    with pytest.raises(ValueError, match="exploration_rate"):
+        PolicyConfig(exploration_rate=0.5)
+    with pytest.raises(ValueError, match="unknown policy fields"):
+        PolicyConfig.from_dict({"bogus": 1})
+    p = PolicyConfig.naive()
+    assert p.k_max == 0 and not p.canary_enabled
+    assert PolicyConfig.from_dict(PolicyConfig().to_dict()) == PolicyConfig()
+    c = PolicyConfig(greedy_value_budget=0.1).to_c()
+    assert c.greedy_value_budget == 0.1 and PolicyConfig().to_c().greedy_value_budget < 0
+
+
+def test_events_from_flags_order():
+    fl = _lib.F_RUNG1 | _lib.F_RUNG2 | _lib.F_RANKING | _lib.F_BOUNDARY | _lib.F_CANARY
+    ev = events_from_flags(fl, 3, 7)
+    assert [(e.rung, e.cause) for e in ev] == [
+        (1, "coverage_expand"), (2, "value_tol"), (3, "ranking_disagree"),
+        (3, "boundary"), (4, "canary")]
+    with pytest.raises(ValueError):
+        FallbackEvent(4, 0, 0, "boundary")
+
+
+def test_certificate_returned_bounds():
+    c = Certificate(0, 0, 0.1, 1.0, 2.0, 0.5, 0.3, 4.0, 8, "dense_per_head", RungFlags(rung3=True))
+    assert c.is_dense and c.returned_e_key == 0.0 and c.returned_e_val == 0.0
+    q = Certificate(0, 0, 0.1, 1.0, 2.0, 0.5, 0.3, 4.0, 8, "quantized")
+    assert q.returned_e_key == 2.0 and q.returned_e_val == 0.5
+
+
+def test_storage_table_matches_oracle():
+    for d, b, g in [(128, 16, 16), (64, 16, 16), (32, 8, 8)]:
+        a = storage_table(d, b, g).to_dict()
+        o = oracle.storage_table(d, b, g)
+        for k, v in o.items():
+            assert a[k] == v, k
+    assert storage_table(128, 16, 16).tier1_total_bytes == _lib.BLOCK_BYTES / _lib.BLOCK
+
+
+def test_synth_arrays_match_oracle_generator():
+    for kind in ("gaussian", "sink", "needle", "near_tie"):
+        cfg = WorkloadConfig(kind=kind, n_tokens=100, head_dim=128, query_heads=8, kv_heads=2,
+                             steps=3, seed=4)
+        k, v, q = synth_arrays(cfg)
+        o = make_workload(kind=kind, n_tokens=100, head_dim=128, query_heads=8, kv_heads=2,
+                          steps=3, seed=4, build_caches=False)
+        assert np.array_equal(k, o["keys"]) and np.array_equal(v, o["values"])
+        assert np.array_equal(q, o["queries"])
+
+
+def test_telemetry_schema_matches_oracle():
+    """A device-shaped record built from certificates aggregates exactly like
+    the oracle's (harness.py:397-499)."""
+    cfg = WorkloadConfig(kind="gaussian", n_tokens=64, head_dim=128, query_heads=4,
+                         kv_heads=1, steps=2)
+    recs = []
+    for s in range(2):
+        certs = [Certificate(h, s, 0.1 * h, 0.01, 0.02 * h, 0.3, 0.2, 3.0, 4 + h,
+                             "quantized" if h else "dense_per_head",
+                             RungFlags(rung3=(h == 0)))
+                 for h in range(4)]
+        ev = [FallbackEvent(3, 0, s, "ranking_disagree")]
+        recs.append(step_record(s, certs, ev, {"hits": 1, "misses": 2, "hit_rate": 1 / 3,
+                                               "bytes_paged_in": 8192},
+                                {"hits": 0, "misses": 0, "hit_rate": 0.0, "bytes_paged_in": 0},
+                                8192, 0, [0.5]))
+    a = aggregate_telemetry(recs, cfg)
+    b = oracle_aggregate(recs, 4)
+    assert a == b
+    assert a["rates"]["dense_fraction"] == 0.25
