@@ -174,6 +174,9 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
 ckv_status ckv_append(const ckv_cache* c, const uint16_t* k_new, const uint16_t* v_new,
                       int32_t n_tok, void* stream);
 
+/* Binary16 ingest of float64 data (correctly rounded, as numpy's astype(float16)). */
+ckv_status ckv_f64_to_f16(const double* x, uint16_t* y, int64_t n, void* stream);
+
 /* Zero a cache's counters (n_blocks, partial_len, v_max, status). */
 ckv_status ckv_reset(const ckv_cache* c, void* stream);
 

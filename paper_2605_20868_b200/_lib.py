@@ -97,6 +97,7 @@ def load():
         "ckv_block_logmass": (I32, [P, P, I32, P, P, P, P]),
         "ckv_fused_attend": (I32, [P, P, P, I32, I32, P, P, P]),
         "ckv_last_launches": (I32, []),
+        "ckv_f64_to_f16": (I32, [P, P, ctypes.c_int64, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -110,7 +111,8 @@ def exported_symbols():
     """Names every entry point declared in include/certkv_b200.h."""
     return ["ckv_version", "ckv_lru_words", "ckv_scratch_init", "ckv_plan", "ckv_append",
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
-            "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches"]
+            "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
+            "ckv_f64_to_f16"]
 
 
 def check(code, what):

@@ -117,8 +117,7 @@ class DeviceKVCache:
         if (self._tokens + n) // B > self.max_blocks:
             raise ValueError(f"append of {n} tokens exceeds the cache capacity "
                              f"({self.max_blocks * B} tokens)")
-        k16 = k.to(torch.float16).contiguous()
-        v16 = v.to(torch.float16).contiguous()
+        k16, v16 = self._to_half(k), self._to_half(v)
         if validate and (k.dtype != torch.float16):
             # a finite fp32/fp64 value can overflow binary16: the reference
             # rejects non-finite inputs before the cast (cache.py:80-81)
@@ -136,6 +135,17 @@ class DeviceKVCache:
                 raise ValueError("cache capacity exceeded")
         self._tokens += n
         self._keep = (k16, v16)  # keep inputs alive until the stream consumes them
+
+    def _to_half(self, x):
+        if x.dtype == torch.float16:
+            return x.contiguous()
+        if x.dtype != torch.float64:
+            return x.float().to(torch.float16).contiguous()  # fp32 -> fp16: one rounding
+        x = x.contiguous()
+        y = torch.empty(x.shape, dtype=torch.float16, device=self.device)
+        code = self.lib.ckv_f64_to_f16(_ptr(x), _ptr(y), x.numel(), _stream(self.device))
+        _lib.check(code, "ckv_f64_to_f16")
+        return y
 
     def reset(self):
         _lib.check(self.lib.ckv_reset(ctypes.byref(self.c), _stream(self.device)), "ckv_reset")

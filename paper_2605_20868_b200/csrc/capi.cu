@@ -8,6 +8,7 @@ cudaError_t launch_read_tier1(const ckv_cache*, int, int, int, int8_t*, float*, 
                               uint16_t*, uint16_t*, cudaStream_t);
 cudaError_t launch_fault_offset(const ckv_cache*, int, int, int, float, cudaStream_t);
 cudaError_t launch_tier2_drop(const ckv_cache*, int, int, cudaStream_t);
+cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
 cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
@@ -135,6 +136,11 @@ ckv_status ckv_fused_attend(const float* scores, const float* values, const int6
                             int32_t nb, int32_t d, float* out, float* ml, void* stream) {
   if (nb < 0 || d <= 0 || d > 1024 || !out || !ml) return CKV_EINVAL;
   return st_of(ckv::launch_fused_attend(scores, values, bounds, nb, d, out, ml, S(stream)));
+}
+
+ckv_status ckv_f64_to_f16(const double* x, uint16_t* y, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !y))) return CKV_EINVAL;
+  return st_of(ckv::launch_f64_to_f16(x, y, (size_t)n, S(stream)));
 }
 
 int32_t ckv_last_launches(void) { return ckv::g_launches; }

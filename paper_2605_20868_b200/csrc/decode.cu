@@ -319,7 +319,7 @@ struct SelSmem {
 };
 
 __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
   uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
   const ckv_cache& c = a.c;
@@ -463,12 +463,9 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       ngt += (k > prefix);
       neq += (k == prefix);
     }
-    int tot_gt, tot_eq;
     const int off_gt = block_excl_scan(ngt, S.wsum, &S.misc[2]);
-    tot_gt = S.misc[2];
+    const int tot_gt = S.misc[2];
     const int off_eq = block_excl_scan(neq, S.wsum, &S.misc[3]);
-    tot_eq = S.misc[3];
-    (void)tot_eq;
     int pg = off_gt, pe = off_eq;
     for (int b = lo_i; b < hi_i; ++b) {
       const uint32_t k = okey(lm[b]);

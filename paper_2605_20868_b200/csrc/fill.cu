@@ -234,6 +234,14 @@ __global__ void k_read_tier1(ckv_cache c, int u, int b0, int8_t* kc, float* ks, 
   }
 }
 
+// binary16 ingest of float64 inputs, rounded once (numpy astype(float16));
+// casting through float32 first would double-round (cache.py:82-84).
+__global__ void k_f64_to_f16(const double* x, uint16_t* y, size_t n) {
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) y[i] = double_to_half_rn(x[i]);
+}
+
 __global__ void k_fault_offset(ckv_cache c, int u, int b, int ch, float shift) {
   float* off = reinterpret_cast<float*>(c.tier1 + ((size_t)u * c.max_blocks + b) * REC + OFF_KOFF);
   off[ch] = off[ch] + shift;
@@ -285,6 +293,13 @@ cudaError_t launch_read_tier1(const ckv_cache* c, int u, int b0, int nb, int8_t*
                               float* ko, uint8_t* vc, uint16_t* vs, uint16_t* vo, cudaStream_t s) {
   if (nb <= 0) return cudaSuccess;
   k_read_tier1<<<nb, 128, 0, s>>>(*c, u, b0, kc, ks, ko, vc, vs, vo);
+  return cudaGetLastError();
+}
+cudaError_t launch_f64_to_f16(const double* x, uint16_t* y, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  size_t g = (n + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  k_f64_to_f16<<<(unsigned)g, 256, 0, s>>>(x, y, n);
   return cudaGetLastError();
 }
 cudaError_t launch_fault_offset(const ckv_cache* c, int u, int b, int ch, float shift,
