@@ -1,0 +1,390 @@
+"""Certified decode-attention steps/s at Llama-3.1-8B attention shape, 128K context.
+
+One step = one full decode step of the model's attention: every (layer, KV
+head) unit (32 layers x 8 KV heads, 4 q-heads each) runs the certified path
+(Phase-1 INT8 scoring, selection + Rung 1/2, page-in accounting, Phase-2
+mask-gated attend, E_key/E_val certificates, ranking/boundary/canary, dense
+fallback for flagged heads) and then appends one new token per unit
+(quantize-on-append).  KV heads are sharded across ranks (N GPUs); per step the
+ranks all-gather outputs + certificates over NCCL.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  `--impl reference` times the CPU oracle port
+of the reference path (oracle/, NumPy) on the host cores instead.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Certified decode-attention steps/s (Llama-3.1-8B, 128K ctx); % HBM peak"
+UNIT = "steps/s"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--kv-heads", type=int, default=8)
+    ap.add_argument("--q-per-kv", type=int, default=4)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--tier2", default="device", choices=["device", "host"])
+    ap.add_argument("--scratch", type=int, default=-1,
+                    help="LRU scratch capacity in blocks (-1: every block, 0: off)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peak_hbm():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = list(self.rows)
+        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
+        smax = float(rows[0][1]) if rows else None
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# -------------------------------------------------------------------------
+# CPU oracle timing (reference arm and cpu_baseline)
+# -------------------------------------------------------------------------
+
+_W = {}
+
+
+def _worker_init(ctx, seed, n_heads):
+    import numpy as np
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    import oracle
+    rng = np.random.default_rng(seed)
+    kv = oracle.OracleKV(16, 128, 16, ingest_binary16=True, narrow=False)
+    kv.append_tokens(rng.standard_normal((ctx, 128)), rng.standard_normal((ctx, 128)))
+    _W.update(kv=kv, rng=rng, n_heads=n_heads)
+
+
+def _worker_step(_):
+    """One unit-step of the reference path: n_heads certified q-heads, then
+    quantize-on-append of the new token (harness.py:351-382)."""
+    import oracle
+    from oracle.step import OraclePolicy
+    kv, rng = _W["kv"], _W["rng"]
+    pol = OraclePolicy(exploration_rate=0.0)
+    t0 = time.perf_counter()
+    for _h in range(_W["n_heads"]):
+        oracle.decode_step(rng.standard_normal(128), kv, pol)
+    kv.append_token(rng.standard_normal(128), rng.standard_normal(128))
+    return time.perf_counter() - t0
+
+
+def cpu_reference(args, total_units, steps, warmup, workers):
+    """Time the oracle port on `workers` host processes; each step runs one
+    unit-step per worker and is scaled to the full step (total_units)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    t_build = time.perf_counter()
+    with ctx.Pool(workers, initializer=_worker_init,
+                  initargs=(args.ctx, 1234, args.q_per_kv)) as pool:
+        pool.map(_worker_step, range(workers))  # make every worker build its cache
+        build_s = time.perf_counter() - t_build
+        for _ in range(warmup):
+            pool.map(_worker_step, range(workers))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pool.map(_worker_step, range(workers))
+        dt = (time.perf_counter() - t0) / steps
+    # one pool round = `workers` unit-steps; a full step needs total_units
+    sec_per_step = dt * total_units / workers
+    return 1.0 / sec_per_step, dt, build_s
+
+
+# -------------------------------------------------------------------------
+# our arm
+# -------------------------------------------------------------------------
+
+def main():
+    args = parse()
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    K, W = args.steps, max(3, args.warmup)
+    total_units = args.layers * args.kv_heads * args.batch
+    config = {"workload": "C3: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, "
+                          f"{args.ctx} ctx, batch {args.batch}, KV-head sharded",
+              "ctx": args.ctx, "layers": args.layers, "kv_heads": args.kv_heads,
+              "q_heads": args.kv_heads * args.q_per_kv, "batch": args.batch,
+              "parallelism": f"kv-head shard x{args.gpus}",
+              "policy": "PolicyConfig(exploration_rate=0.0) defaults",
+              "l2": "inputs larger than L2 (Tier-1 9.66 GB/step at 128K)",
+              "tier2": args.tier2}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        try:
+            ncpu = len(os.sched_getaffinity(0))
+        except Exception:
+            ncpu = os.cpu_count() or 1
+        workers = max(1, min(ncpu, 16))
+        rate, dt, build_s = cpu_reference(args, total_units, K, W, workers)
+        line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+                "warmup": W, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
+                                 "sample": f"{workers} of {total_units} units (one per process) "
+                                           f"at {args.ctx} ctx, {args.q_per_kv} q-heads each, "
+                                           f"per step; scaled x{total_units / workers:.1f}"},
+                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2605_20868_b200 as ck
+    from paper_2605_20868_b200 import _lib
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    # KV-head sharding: units are kv-major (u = kv * layers*batch + layer*batch + seq)
+    if args.kv_heads % world:
+        raise SystemExit("kv_heads must be divisible by the number of GPUs")
+    per = total_units // world
+    U = per
+    max_tokens = args.ctx + 2 * (K + W) + 32
+    cache = ck.DeviceKVCache(U, max_tokens, device=dev, tier2=args.tier2)
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    chunk = 4096
+    t0 = time.perf_counter()
+    for pos in range(0, args.ctx, chunk):
+        n = min(chunk, args.ctx - pos)
+        kk = torch.randn((U, n, 128), generator=g, device=dev).half()
+        vv = torch.randn((U, n, 128), generator=g, device=dev).half()
+        cache.append(kk, vv, validate=False)
+    torch.cuda.synchronize()
+    prefill_s = time.perf_counter() - t0
+
+    pol = ck.PolicyConfig(exploration_rate=0.0)
+    cap = cache.max_blocks if args.scratch < 0 else args.scratch
+    scratch = ck.ScratchCache(cap) if args.scratch != 0 else None
+    group = args.kv_heads // world  # units sharing a layer's step-wide rung 4 (local part)
+    dec = ck.CertifiedDecoder(cache, pol, n_heads=args.q_per_kv, scratch=scratch,
+                              rung4_group=None)
+    nq = W + K
+    qpool = torch.randn((nq, U, args.q_per_kv, 128), generator=g, device=dev, dtype=torch.float64)
+    kpool = torch.randn((nq, U, 1, 128), generator=g, device=dev).half()
+    vpool = torch.randn((nq, U, 1, 128), generator=g, device=dev).half()
+    ev_a = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(K)]
+    for a, b in ev_a:  # torch creates the CUDA event lazily: force it before handing it over
+        a.record()
+        b.record()
+    gather_bytes = U * args.q_per_kv * (128 * 4 + 88)
+    gbuf = torch.empty(gather_bytes * world, dtype=torch.uint8, device=dev)
+
+    def exchange():
+        if world == 1:
+            return
+        # outputs + certificates -> every rank (the bound report), one NCCL call
+        local_buf = torch.cat([dec.out.view(torch.uint8).reshape(-1),
+                               dec.cert_buf.reshape(-1)])
+        dist.all_gather_into_tensor(gbuf, local_buf)
+
+    launches = {"n": 0}
+    dense_heads = {"n": 0}
+
+    def one_step(i, timed_ev=None):
+        if timed_ev is not None:
+            dec.st.prof_begin = timed_ev[0].cuda_event
+            dec.st.prof_end = timed_ev[1].cuda_event
+        res = dec.step(qpool[i])
+        dec.st.prof_begin = None
+        dec.st.prof_end = None
+        launches["n"] += lib.ckv_last_launches()
+        dense_heads["n"] += int((res.kinds != 0).sum())
+        exchange()
+        cache.append(kpool[i], vpool[i], validate=False)
+        launches["n"] += lib.ckv_last_launches()
+        return res
+
+    lib = cache.lib
+    for i in range(W):
+        one_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    launches["n"] = 0
+    dense_heads["n"] = 0
+    nb_timed = cache.num_blocks
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_start.record()
+    for i in range(K):
+        one_step(W + i, ev_a[i])
+    t_end.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end) / K
+    pa_ms = sum(a.elapsed_time(b) for a, b in ev_a) / K
+    clocks = sampler.stop() if sampler else None
+    n_launch = launches["n"]
+    n_dense = dense_heads["n"]
+    if world > 1:
+        t = torch.tensor([ms, pa_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, pa_ms = float(t[0]), float(t[1])
+
+    # ---- end to end through the public API with host buffers -----------------
+    e2e = None
+    if not args.no_e2e:
+        qh = torch.randn((K, U, args.q_per_kv, 128), dtype=torch.float64).pin_memory()
+        kh = torch.randn((K, U, 1, 128)).half().pin_memory()
+        vh = torch.randn((K, U, 1, 128)).half().pin_memory()
+        oh = torch.empty((U, args.q_per_kv, 128), dtype=torch.float32).pin_memory()
+        for i in range(2):  # warm the pinned paths
+            dec.step(qh[i].to(dev, non_blocking=True))
+            oh.copy_(dec.out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = time.perf_counter()
+        for i in range(K):
+            res = dec.step(qh[i].to(dev, non_blocking=True))
+            exchange()
+            oh.copy_(dec.out, non_blocking=True)
+            cache.append(kh[i].to(dev, non_blocking=True), vh[i].to(dev, non_blocking=True))
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - e0) * 1000.0 / K
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        h2d = qh[0].numel() * 8 + kh[0].numel() * 2 + vh[0].numel() * 2
+        d2h = oh.numel() * 4 + dec.cert_buf.numel()
+        e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peak_hbm()
+    tier1_bytes_launch = U * nb_timed * _lib.BLOCK_BYTES  # Tier-1 read by one pass A
+    achieved = tier1_bytes_launch / (pa_ms / 1000.0) / 1e9
+    step_bytes = total_units * args.ctx * 288.0
+    step_frac = step_bytes / (ms / 1000.0) / 1e9 / peak
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "pass_a_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rate, dt, _ = cpu_reference(args, total_units, 2, 1, 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"1 of {total_units} units at {args.ctx} ctx ({args.q_per_kv} q-heads "
+                         f"+ append), 2 timed unit-steps on one core, scaled x{total_units}"}
+
+    value = 1000.0 / ms
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int8/int4 codes, fp32 accumulate", "data": "synthetic",
+        "config": config,
+        "hbm_frac_step": step_frac,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_pass_a (Tier-1 stream, Phase 1 + speculative Phase 2)",
+                     "peak_kind": peak_kind, "pass_a_ms": pa_ms},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_launch,
+        "dense_heads_in_timed_region": n_dense,
+        "clocks": clocks,
+        "prefill_s": prefill_s,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

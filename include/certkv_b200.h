@@ -145,6 +145,8 @@ typedef struct {
   float* head_state;        /* [n_units][n_heads][CKV_HEAD_FLOATS] */
   float* chunk_state;       /* [n_units][n_heads][n_chunks][CKV_CHUNK_FLOATS] */
   int32_t* page_stats;      /* [n_units][4] key hits, key misses, value hits, value misses */
+  void* prof_begin;         /* optional cudaEvent_t recorded before / after pass A */
+  void* prof_end;
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136

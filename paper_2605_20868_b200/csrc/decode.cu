@@ -1009,10 +1009,12 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
     attrs = true;
   }
   const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
+  if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
   if (nsplit_used > 0) {
     k_pass_a<<<dim3(nsplit_used, c->n_units), PA_WARPS * 32, smA, s>>>(a);
     ++g_launches;
   }
+  if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   k_select<<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
