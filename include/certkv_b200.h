@@ -147,6 +147,10 @@ typedef struct {
   int32_t* page_stats;      /* [n_units][4] key hits, key misses, value hits, value misses */
   void* prof_begin;         /* optional cudaEvent_t recorded before / after pass A */
   void* prof_end;
+  int32_t rung4_group;      /* units sharing a step-wide rung 4 (0 = all units) */
+  int32_t n_dsplit_cap;     /* dense-fallback splits per unit (from ckv_plan) */
+  int32_t* dense_list;      /* [1 + n_units] count, then unit | head_mask << 24 */
+  float* dense_part;        /* [n_units][n_dsplit_cap][4][132] dense split states */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136

@@ -59,7 +59,8 @@ class CkvStep(ctypes.Structure):
                 ("wcap", I32), ("n_chunks", I32), ("items_per_chunk", I32), ("q", P),
                 ("out", P), ("cert", P), ("lm1", P), ("split_state", P), ("order", P),
                 ("work", P), ("n_work", P), ("vlist", P), ("lm2", P), ("head_state", P),
-                ("chunk_state", P), ("page_stats", P), ("prof_begin", P), ("prof_end", P)]
+                ("chunk_state", P), ("page_stats", P), ("prof_begin", P), ("prof_end", P),
+                ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P)]
 
 
 class CkvScratch(ctypes.Structure):

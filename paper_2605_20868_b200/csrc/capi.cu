@@ -11,6 +11,7 @@ cudaError_t launch_tier2_drop(const ckv_cache*, int, int, cudaStream_t);
 cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
 cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_dense(const ckv_cache*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
 int lru_ring(int, int);
@@ -68,6 +69,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->items_per_chunk = 32;
   st->n_chunks = (st->kcap + 31) / 32;
   if (st->n_chunks < 1) st->n_chunks = 1;
+  st->n_dsplit_cap = (max_blocks * CKV_BLOCK + CKV_BLOCK + 2047) / 2048;
   return CKV_OK;
 }
 
@@ -87,11 +89,13 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
   if (!cache_ok(c) || !pol || !st || !st->q || !st->out || !st->cert || !st->lm1 ||
       !st->split_state || !st->order || !st->work || !st->n_work || !st->vlist || !st->lm2 ||
-      !st->head_state || !st->chunk_state)
+      !st->head_state || !st->chunk_state || !st->dense_list || !st->dense_part)
     return CKV_EINVAL;
   if (host_max_blocks < 0 || host_max_blocks > c->max_blocks) return CKV_EINVAL;
   if (pol->greedy_value_budget >= 0.0) return CKV_EINVAL;  // greedy rung 2 not on device yet
   cudaError_t e = ckv::launch_decode(c, pol, st, host_max_blocks, S(stream));
+  if (e != cudaSuccess) return CKV_ECUDA;
+  e = ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream));
   if (e != cudaSuccess) return CKV_ECUDA;
   if (scratch) {
     if (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters)

@@ -1,11 +1,10 @@
 """Certified decode step driver (host side of the C ABI) and the reference API.
 
 ``CertifiedDecoder.step`` is the batched certified attention call: one C call
-launches pass A / select / pass B / combine (+ the LRU scratch accounting)
-for every (unit, q-head); the host then reads back the certificate array,
-resolves step-wide Rung 4 (harness.py:362-372) and runs the terminal dense
-fallback with ``scaled_dot_product_attention`` over the FP16 Tier-2 originals
-for the flagged heads only.
+launches pass A / select / pass B / combine, the step-wide Rung 4 resolution
+(harness.py:362-372), the terminal dense fallback (exact fp32 attention over
+the FP16 Tier-2 originals, flagged units only) and the LRU scratch accounting
+for every (unit, q-head); the host then reads back the certificate array.
 
 ``run_decode_step`` / ``run_workload`` keep the reference signatures
 (harness.py:186-394) on top of it.
@@ -17,7 +16,6 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import torch
-import torch.nn.functional as F
 
 from . import _lib
 from .cache import DeviceKVCache, ScratchCache, TieredCache, _ptr, _stream
@@ -89,18 +87,22 @@ class CertifiedDecoder:
         self.chunk_state = torch.zeros((U, nh, st.n_chunks, _lib.CHUNK_FLOATS),
                                        dtype=torch.float32, device=dev)
         self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
+        self.dense_list = torch.zeros((U + 1,), dtype=torch.int32, device=dev)
+        self.dense_part = torch.zeros((U, st.n_dsplit_cap, 4, 132), dtype=torch.float32, device=dev)
         for name, t in (("q", self.q), ("out", self.out), ("cert", self.cert_buf),
                         ("lm1", self.lm1), ("split_state", self.split_state),
                         ("order", self.order), ("work", self.work), ("n_work", self.n_work),
                         ("vlist", self.vlist), ("lm2", self.lm2),
                         ("head_state", self.head_state), ("chunk_state", self.chunk_state),
-                        ("page_stats", self.page_stats)):
+                        ("page_stats", self.page_stats), ("dense_list", self.dense_list),
+                        ("dense_part", self.dense_part)):
             setattr(st, name, _ptr(t))
+        self.rung4_group = int(rung4_group or U)
+        st.rung4_group = self.rung4_group
         self.st = st
         self.scratch = scratch
         if scratch is not None:
             scratch.bind(cache)
-        self.rung4_group = int(rung4_group or U)
         self.cert_host = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
 
     # -- the device step -----------------------------------------------------
@@ -114,8 +116,13 @@ class CertifiedDecoder:
                                         _stream(self.cache.device))
         _lib.check(code, "ckv_decode_step")
 
-    def step(self, queries, dense=True):
-        """Certified attention for all units: queries [U, nh, 128] (float64)."""
+    def step(self, queries):
+        """Certified attention for all units: queries [U, nh, 128] (float64).
+
+        The fast path, the step-wide Rung 4 resolution and the dense fallback
+        all run on the device inside one ``ckv_decode_step``; the host reads
+        back the certificate array (and raises on a Tier-2 loss).
+        """
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
         if self.policy.exploration_rate > 0:
@@ -131,31 +138,12 @@ class CertifiedDecoder:
         cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh).copy()
         kinds = cert["returned_kind"].copy()
         U, g = self.cache.n_units, self.rung4_group
-        r4 = (kinds == 2).any(axis=1)
         staging = 0
         for g0 in range(0, U, g):
-            if r4[g0:g0 + g].any():
-                kinds[g0:g0 + g, :] = 2
-                staging += sum(2 * self.cache.num_tokens * D * 2 for _ in range(min(g, U - g0)))
-        if dense:
-            self.dense_fallback(kinds)
+            if (kinds[g0:g0 + g] == 2).any():
+                staging += min(g, U - g0) * 2 * self.cache.num_tokens * D * 2
         ps = self.page_stats.cpu().numpy().copy() if self.scratch is not None else None
         return StepOutput(self.out, cert, kinds, ps, staging, self)
-
-    def dense_fallback(self, kinds):
-        """Rung 3/4: exact attention over the FP16 originals (attention.py:327-342)
-        with scaled_dot_product_attention, for flagged units only."""
-        units = np.nonzero((kinds != 0).any(axis=1))[0]
-        for u in units:
-            u = int(u)
-            self.cache.check_tier2(u)
-            k, v = self.cache.tier2_rows(u)
-            heads = np.nonzero(kinds[u] != 0)[0]
-            q = self.q[u, torch.as_tensor(heads, device=self.q.device)].float()
-            o = F.scaled_dot_product_attention(
-                q[None, :, None, :], k.float()[None, None].expand(1, len(heads), -1, -1),
-                v.float()[None, None].expand(1, len(heads), -1, -1))
-            self.out[u, torch.as_tensor(heads, device=self.q.device)] = o[0, :, 0, :]
 
 
 # -- reference-shaped per-head API --------------------------------------------
