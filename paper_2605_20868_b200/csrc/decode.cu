@@ -112,11 +112,9 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
   const int h = lane & 3;
   const int t0 = lane >> 2, t1 = t0 + 8;
   float m_run = ninf(), l_run = 0.f, dmax = 0.f;
-  float o[H][4];
+  float2 o2[H][2];
 #pragma unroll
-  for (int i = 0; i < H; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[i][j] = 0.f;
+  for (int i = 0; i < H; ++i) o2[i][0] = o2[i][1] = make_float2(0.f, 0.f);
 
   float* lm1 = st.lm1 + ((size_t)u * nh + (h < nh ? h : 0)) * c.max_blocks;
   const int g = lane >> 2;  // value group of the lane's channels
@@ -153,12 +151,17 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
     __syncwarp();
 
     // ---- speculative phase 2: INT4 values, lane owns channels 4l..4l+3 --------
-    const float4 al = *reinterpret_cast<const float4*>(S.abuf[warp]);
-    const float alv[4] = {al.x, al.y, al.z, al.w};
+    // packed fp32x2 FMAs (FFMA2): channel pairs (0,1) and (2,3)
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
+      const float4 al = *reinterpret_cast<const float4*>(S.abuf[warp]);
+      const float alv[4] = {al.x, al.y, al.z, al.w};
 #pragma unroll
-    for (int hh = 0; hh < H; ++hh)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[hh][j] *= alv[hh];
+      for (int hh = 0; hh < H; ++hh) {
+        const float2 a2 = make_float2(alv[hh], alv[hh]);
+        o2[hh][0] = __fmul2_rn(o2[hh][0], a2);
+        o2[hh][1] = __fmul2_rn(o2[hh][1], a2);
+      }
+    }
     const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
     const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
     const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
@@ -173,20 +176,24 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
         const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
         const __half2 so = *reinterpret_cast<const __half2*>(&mv[k]);
         const float2 sof = __half22float2(so);
-        const float s16 = 16.f * sof.x;
+        // v = u*s + o = (16 + u)*s + (o - 16 s); 16 + u is the float with
+        // exponent 4 and the nibble in the top mantissa bits
         const float op = fmaf(-16.f, sof.x, sof.y);
-        float v[4];
+        float fb[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t bits = ((cw << (19 - 4 * j)) & 0x00780000u) | 0x3F800000u;
-          v[j] = fmaf(__uint_as_float(bits), s16, op);
-        }
+        for (int j = 0; j < 4; ++j)
+          fb[j] = __uint_as_float(((cw << (19 - 4 * j)) & 0x00780000u) | 0x41800000u);
+        const float2 s2 = make_float2(sof.x, sof.x), o2c = make_float2(op, op);
+        const float2 v01 = __ffma2_rn(make_float2(fb[0], fb[1]), s2, o2c);
+        const float2 v23 = __ffma2_rn(make_float2(fb[2], fb[3]), s2, o2c);
         const float4 p4 = *reinterpret_cast<const float4*>(S.pbuf[warp][t]);
         const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
-        for (int hh = 0; hh < H; ++hh)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) o[hh][j] = fmaf(pv[hh], v[j], o[hh][j]);
+        for (int hh = 0; hh < H; ++hh) {
+          const float2 pp = make_float2(pv[hh], pv[hh]);
+          o2[hh][0] = __ffma2_rn(pp, v01, o2[hh][0]);
+          o2[hh][1] = __ffma2_rn(pp, v23, o2[hh][1]);
+        }
       }
     }
     __syncwarp();
@@ -208,9 +215,12 @@ __global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
     mw[(warp * H + lane) * 4 + 2] = dmax;
   }
 #pragma unroll
-  for (int hh = 0; hh < H; ++hh)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) ow[(warp * H + hh) * D + lane * 4 + j] = o[hh][j];
+  for (int hh = 0; hh < H; ++hh) {
+    ow[(warp * H + hh) * D + lane * 4 + 0] = o2[hh][0].x;
+    ow[(warp * H + hh) * D + lane * 4 + 1] = o2[hh][0].y;
+    ow[(warp * H + hh) * D + lane * 4 + 2] = o2[hh][1].x;
+    ow[(warp * H + hh) * D + lane * 4 + 3] = o2[hh][1].y;
+  }
   __syncthreads();
   const int ch = tid;  // 128 threads = 128 channels
   for (int hh = 0; hh < H; ++hh) {

@@ -29,7 +29,8 @@ __device__ __forceinline__ int bchan(int lane, int kt, int j) {
   return kt * 32 + (lane & 3) * 4 + (j & 3) + ((j >> 2) << 4);
 }
 
-__device__ __forceinline__ float pow2f(int e) {  // exact 2^e for e in [-126, 127]
+__device__ __forceinline__ float pow2f(int e) {  // exact 2^e, e clamped to the normal range
+  e = max(-126, min(127, e));
   return __uint_as_float((uint32_t)(e + 127) << 23);
 }
 
@@ -46,7 +47,7 @@ __device__ inline void load_qfrag(QFrag& f, const float* qh, int lane) {
     if (h == (lane & 3)) f.eq_l = e;
     if (h == hb) eq_b = e;
   }
-  const float sc = ldexpf(1.0f, 21 - eq_b);
+  const float sc = pow2f(21 - eq_b);
   const bool odd = (lane >> 2) & 1;
 #pragma unroll
   for (int kt = 0; kt < 4; ++kt) {
@@ -72,9 +73,12 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
   const bool odd = (lane >> 2) & 1;
   const float* aux = odd ? zz : sig;  // per-lane operand for the Delta / constz sums
   const int es = ilogbf(smax) + 1;    // smax < 2^es
-  const float sdown = ldexpf(1.0f, -es);
+  // fma(qsc, sigma, 1.5*2^(23+es)) has the same mantissa bits as
+  // fma(qsc, sigma*2^-es, 1.5*2^23) (exact power-of-two scaling): the bytes of
+  // U = X + 2^22 come out unchanged, except that byte 2 carries the exponent
+  // LSB (es & 1) in its top bit, removed below with the sum-of-codes column.
+  const float magic_b = __uint_as_float(((uint32_t)(150 + es) << 23) | 0x400000u);
   const uint32_t sel0 = ((lane >> 2) & 1) ? 0x5151u : 0x4040u;  // byte 1 or 0 of y0,y1
-  const float MAGIC = 12582912.0f;  // 1.5 * 2^23
   int d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
   float acc = 0.f;
 #pragma unroll
@@ -89,7 +93,7 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
     uint32_t y[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      y[j] = __float_as_uint(fmaf(f.qsc[kt * 8 + j], sv[j] * sdown, MAGIC));
+      y[j] = __float_as_uint(fmaf(f.qsc[kt * 8 + j], sv[j], magic_b));
       acc = fmaf(f.aw[kt * 8 + j], xv[j], acc);
     }
     // tile 0: byte (lane/4)&1 of the four U values, packed into one register
@@ -112,18 +116,19 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
   const int h = lane & 3;
   const float dsum = __shfl_sync(0xffffffffu, acc, h * 8);      // sum |qsc| sigma (head h)
   const float zsum = __shfl_sync(0xffffffffu, acc, h * 8 + 4);  // sum qsc z (head h)
-  const float inv_q = ldexpf(1.0f, f.eq_l - 21);
-  const float scl = ldexpf(1.0f, f.eq_l + es - 21);
+  const float inv_q = pow2f(f.eq_l - 21);
+  const float scl = pow2f(f.eq_l + es - 21);
   const float constz = zsum * inv_q;
+  const int bias = 64 + ((es & 1) << 7);
   BlockScores r;
   {
     int lo = d0[0] + 256 * d0[1];
-    int hi = d1[0] - 64 * d1[1];
+    int hi = d1[0] - bias * d1[1];
     r.s0 = fmaf(fmaf((float)hi, 65536.f, (float)lo), scl, constz);
   }
   {
     int lo = d0[2] + 256 * d0[3];
-    int hi = d1[2] - 64 * d1[3];
+    int hi = d1[2] - bias * d1[3];
     r.s1 = fmaf(fmaf((float)hi, 65536.f, (float)lo), scl, constz);
   }
   r.delta = 0.5f * dsum * inv_q;
