@@ -138,12 +138,12 @@ typedef struct {
   float* lm1;               /* [n_units][n_heads][max_blocks] phase-1 block log-mass */
   float* split_state;       /* [n_units][n_splits][4][CKV_SPLIT_FLOATS] */
   int32_t* order;           /* [n_units][n_heads][kcap] promoted blocks in mass order */
-  int32_t* work;            /* [n_units][n_heads][wcap] (block<<2 | inF | inV<<1) */
-  int32_t* n_work;          /* [n_units][n_heads] */
+  int32_t* work;            /* [n_units][wcap] union work list: block | F-mask<<24 | V-mask<<28 */
+  int32_t* n_work;          /* [n_units] */
   int32_t* vlist;           /* [n_units][n_heads][max_blocks] value promotions, ascending */
-  float* lm2;               /* [n_units][n_heads][kcap] phase-2 log-mass of promoted blocks (order) */
+  float* lm2;               /* [n_units][n_heads][max_blocks] phase-2 log-mass of promoted blocks */
   float* head_state;        /* [n_units][n_heads][CKV_HEAD_FLOATS] */
-  float* chunk_state;       /* [n_units][n_heads][n_chunks][CKV_CHUNK_FLOATS] */
+  float* chunk_state;       /* [n_units][n_chunks][4][CKV_CHUNK_FLOATS] */
   int32_t* page_stats;      /* [n_units][4] key hits, key misses, value hits, value misses */
   void* prof_begin;         /* optional cudaEvent_t recorded before / after pass A */
   void* prof_end;

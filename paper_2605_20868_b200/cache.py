@@ -23,6 +23,20 @@ from .errors import Tier2UnavailableError
 D, B, G = _lib.HEAD_DIM, _lib.BLOCK, _lib.GROUP
 
 
+def _k2_index():
+    """natural [t][c] -> position in the fragment-ordered Tier-2 key block
+    (k2_offset in csrc/common.cuh)."""
+    t = np.arange(B)[:, None]
+    c = np.arange(D)[None, :]
+    kt, cc = c >> 4, c & 15
+    lane = (t & 7) * 4 + ((cc & 7) >> 1)
+    reg = (t >> 3) + 2 * (cc >> 3)
+    return (kt * 256 + lane * 8 + reg * 2 + (cc & 1)).reshape(-1)
+
+
+K2_INDEX = _k2_index()
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -200,6 +214,8 @@ class DeviceKVCache:
         if self.tier2_location == "host":
             k = k.to(self.device, non_blocking=True)
             v = v.to(self.device, non_blocking=True)
+        idx = torch.as_tensor(K2_INDEX, device=k.device)
+        k = k.reshape(-1, B * D)[:, idx].reshape(-1, D)  # fragment order -> [token][channel]
         p = self.partial_len
         if p:
             k = torch.cat([k, self.partial_k[unit, :p]], 0)

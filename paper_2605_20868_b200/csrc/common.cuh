@@ -43,6 +43,19 @@ __host__ __device__ inline int vcode_offset(int t, int c) {  // byte holding cha
 }
 __host__ __device__ inline int vmeta_offset(int t, int g) { return OFF_VMETA + (g * 16 + t) * 4; }
 
+// Tier-2 keys are stored per 16-token block in mma.m16n8k16 (fp16) A-fragment
+// order, so the original-key scores of a block are 8 tensor-core MMAs fed by
+// one coalesced 16-byte load per lane per k-tile: element (t, c) of a block
+// sits at half index  kt*256 + lane*8 + reg*2 + (cc&1)  with kt = c/16,
+// cc = c%16, lane = (t%8)*4 + (cc%8)/2, reg = t/8 + 2*(cc/8).  Tier-2 values
+// keep the natural [token][channel] order.
+__host__ __device__ inline int k2_offset(int t, int c) {
+  int kt = c >> 4, cc = c & 15;
+  int lane = (t & 7) * 4 + ((cc & 7) >> 1);
+  int reg = (t >> 3) + 2 * (cc >> 3);
+  return kt * 256 + lane * 8 + reg * 2 + (cc & 1);
+}
+
 // ---- bit helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
@@ -145,6 +158,15 @@ __device__ __forceinline__ void mma_s8u8(int (&d)[4], const uint4& a, uint32_t b
       "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};"
       : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+// fp16 MMA: D(16x8,f32) += A(16x16,f16) * B(16x8,f16)
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 

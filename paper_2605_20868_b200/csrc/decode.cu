@@ -18,41 +18,9 @@
 // Every additive decomposition is over blocks, so the result equals the
 // reference's single mask-gated pass (attention.py:227-300) up to fp32
 // rounding.
-#include "phase1.cuh"
+#include "step.cuh"
 
 namespace ckv {
-
-struct HeadState {
-  double lse;          // phase-1 log-sum-exp over full blocks + partial
-  double alpha_hat;    // estimated tail mass (non-promoted full blocks)
-  double e_tail;       // sum over b not in F u V of p_b eta_b
-  double partial_mass;
-  float mA, lA;        // merged pass-A softmax state
-  float delta;         // Delta_h
-  float tailmax;       // max phase-1 log-mass over the tail (-inf if empty)
-  float mp, lp;        // partial block state
-  int32_t kprime;      // |F| after rung 1
-  int32_t kstar0;      // K* before rung 1
-  int32_t n_v;
-  int32_t k_cov;
-  int32_t pad[2];
-  float oA[D];
-  float np_[D];
-};
-static_assert(sizeof(HeadState) <= CKV_HEAD_FLOATS * 4, "head state too large");
-
-struct StepArgs {
-  ckv_cache c;
-  ckv_step st;
-  ckv_policy pol;
-};
-
-__device__ __forceinline__ float ninf() { return __int_as_float(0xff800000); }
-
-__device__ __forceinline__ uint32_t okey(float x) {  // order-preserving float -> u32
-  uint32_t b = __float_as_uint(x);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
 
 // =============================================================================
 // pass A
@@ -586,28 +554,18 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   at = block_sum_d(at, S.redd);
   et = block_sum_d(et, S.redd);
   const int vo = block_excl_scan(nv, S.wsum, &S.misc[7]);
-  const int xo = block_excl_scan(nvx, S.wsum, &S.misc[8]);
-  const int n_v = S.misc[7], n_vx = S.misc[8];
+  const int n_v = S.misc[7];
+  (void)nvx;
   {
     int32_t* vlist = st.vlist + hu * c.max_blocks;
-    int32_t* work = st.work + hu * st.wcap;
-    int pv = vo, px = xo;
+    int pv = vo;
     for (int b = lo_i; b < hi_i; ++b) {
       const double pb = exp((double)lm[b] - lse);
-      const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
       const bool inV = r2 && (pb * (double)eta[b] > pol.v_tol);
       if (inV) vlist[pv++] = b;
-      if (inV && !inF) work[kp + px++] = (b << 2) | 2;
-    }
-    for (int i = tid; i < kp; i += SEL_THREADS) {
-      const int b = order[i];
-      const double pb = exp((double)lm[b] - lse);
-      const bool inV = r2 && (pb * (double)eta[b] > pol.v_tol);
-      work[i] = (b << 2) | 1 | (inV ? 2 : 0);
     }
   }
   if (tid == 0) {
-    st.n_work[hu] = kp + n_vx;
     hs.lse = lse;
     hs.alpha_hat = (kp >= nb) ? 0.0 : at;
     hs.e_tail = et;
@@ -634,325 +592,6 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     if (n_v > 0) fl |= CKV_F_RUNG2;
     if (kcov != kstar) fl |= CKV_F_CLAMPED;
     ct.flags = fl;
-  }
-}
-
-// =============================================================================
-// pass B
-// =============================================================================
-constexpr int PB_WARPS = 4;
-
-struct PassBSmem {
-  uint8_t rec[PB_WARPS][REC];
-  float qh[H * D];
-  float sq[PB_WARPS][B];
-  float so[PB_WARPS][B];
-  float mrg[PB_WARPS][8];
-  double mrgd[PB_WARPS][2];
-};
-
-__global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
-  const ckv_cache& c = a.c;
-  const ckv_step& st = a.st;
-  const int ck = blockIdx.x, h = blockIdx.y, u = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nh = st.n_heads;
-  const size_t hu = (size_t)u * nh + h;
-  const int nwork = st.n_work[hu];
-  const int C = gridDim.x;
-  const int ipc = st.items_per_chunk;
-  float* cs = st.chunk_state + (hu * C + ck) * CKV_CHUNK_FLOATS;
-  if (ck * ipc >= nwork) {
-    if (tid == 0) cs[0] = ninf();
-    return;
-  }
-  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
-  for (int i = tid; i < H * D; i += blockDim.x) {
-    int hh = i / D;
-    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
-                        : 0.f;
-  }
-  __syncthreads();
-  QFrag f;
-  load_qfrag(f, S.qh, lane);
-
-  const float* qme = S.qh + h * D;
-  const float* eta = c.eta + (size_t)u * c.max_blocks;
-  const int32_t* work = st.work + hu * st.wcap;
-  float* lm2 = st.lm2 + hu * st.kcap;
-  const double lse = hs.lse;
-  float m_c = hs.mA;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  float dden = 0.f, canary = 0.f;
-  double eF = 0.0, sF = 0.0;
-  const int g = lane >> 2;
-  const size_t ub = (size_t)u * c.max_blocks;
-
-  for (int base = ck * ipc; base < nwork; base += C * ipc) {
-    const int end = min(nwork, base + ipc);
-    for (int it = base + warp; it < end; it += PB_WARPS) {
-      const int e = work[it];
-      const int b = e >> 2;
-      const bool inF = e & 1, inV = (e >> 1) & 1;
-      // stage the Tier-1 record
-      const uint4* src = reinterpret_cast<const uint4*>(c.tier1 + (ub + b) * REC);
-      uint4* dst = reinterpret_cast<uint4*>(S.rec[warp]);
-      for (int k = lane; k < REC / 16; k += 32) dst[k] = src[k];
-      __syncwarp();
-      const uint8_t* rec = S.rec[warp];
-      BlockScores r = phase1_block(f, rec, c.kscale_max[ub + b], lane);
-      if ((lane & 3) == h) {
-        S.sq[warp][lane >> 2] = r.s0;
-        S.sq[warp][(lane >> 2) + 8] = r.s1;
-      }
-      if (inF || inV) {
-        if (!c.tier2_valid[ub + b] && lane == 0) atomicOr(&c.status[CKV_ST_TIER2], 1);
-      }
-      if (inF) {  // original-key scores: two lanes per token, 64 channels each
-        const int t = lane >> 1, hf = lane & 1;
-        const uint4* kp = reinterpret_cast<const uint4*>(c.tier2_k + ((ub + b) * B + t) * D + hf * 64);
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint4 w = kp[k];
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&ww[j]));
-            s = fmaf(kf.x, qme[hf * 64 + k * 8 + 2 * j], s);
-            s = fmaf(kf.y, qme[hf * 64 + k * 8 + 2 * j + 1], s);
-          }
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        if (hf == 0) S.so[warp][t] = s;
-      }
-      __syncwarp();
-      float sn[B], sq[B];
-      float mx = ninf();
-#pragma unroll
-      for (int t = 0; t < B; ++t) {
-        sq[t] = S.sq[warp][t];
-        sn[t] = inF ? S.so[warp][t] : sq[t];
-        mx = fmaxf(mx, sn[t]);
-      }
-      const float m_new = fmaxf(m_c, mx);
-      const float resc = fast_exp(m_c - m_new);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] *= resc;
-      dden *= resc;
-      m_c = m_new;
-      if (inF) {
-        float bm = ninf(), gap = 0.f;
-#pragma unroll
-        for (int t = 0; t < B; ++t) {
-          bm = fmaxf(bm, sn[t]);
-          gap = fmaxf(gap, fabsf(sn[t] - sq[t]));
-        }
-        float bsum = 0.f;
-#pragma unroll
-        for (int t = 0; t < B; ++t) bsum += expf(sn[t] - bm);
-        const float lb = bm + logf(bsum);
-        canary = fmaxf(canary, gap);
-        if (lane == 0) lm2[it] = lb;
-        const double rb = exp((double)lb - lse);
-        sF += rb;
-        if (!inV) eF += rb * (double)eta[b];
-      }
-      // values: lane owns channels 4*lane .. 4*lane+3
-      const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
-      const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-      const uint32_t* vm = reinterpret_cast<const uint32_t*>(rec + OFF_VMETA + g * 64);
-      const uint16_t* vorig = c.tier2_v + (ub + b) * B * D + lane * 4;
-#pragma unroll
-      for (int t = 0; t < B; ++t) {
-        const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
-        const uint32_t mm = vm[t];
-        const float2 sof = __half22float2(*reinterpret_cast<const __half2*>(&mm));
-        const float s16 = 16.f * sof.x;
-        const float op = fmaf(-16.f, sof.x, sof.y);
-        float vq[4], vn[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t bits = ((cw << (19 - 4 * j)) & 0x00780000u) | 0x3F800000u;
-          vq[j] = fmaf(__uint_as_float(bits), s16, op);
-          vn[j] = vq[j];
-        }
-        if (inV) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
-          const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-          const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-          vn[0] = a0.x;
-          vn[1] = a0.y;
-          vn[2] = a1.x;
-          vn[3] = a1.y;
-        }
-        const float wq = expf(sq[t] - m_c);
-        if (inF) {
-          const float wn = expf(sn[t] - m_c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] += wn * vn[j] - wq * vq[j];
-          dden += wn - wq;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] = fmaf(wq, vn[j] - vq[j], acc[j]);
-        }
-      }
-      __syncwarp();
-    }
-  }
-  // ---- merge warps -------------------------------------------------------------------
-  if (lane == 0) {
-    S.mrg[warp][0] = m_c;
-    S.mrg[warp][1] = dden;
-    S.mrg[warp][2] = canary;
-    S.mrgd[warp][0] = eF;
-    S.mrgd[warp][1] = sF;
-  }
-  __syncthreads();
-  float* accs = reinterpret_cast<float*>(S.rec);  // [warp][D]
-#pragma unroll
-  for (int j = 0; j < 4; ++j) accs[warp * D + lane * 4 + j] = acc[j];
-  __syncthreads();
-  float M = ninf();
-  for (int w = 0; w < PB_WARPS; ++w) M = fmaxf(M, S.mrg[w][0]);
-  float O = 0.f, DD = 0.f;
-  for (int w = 0; w < PB_WARPS; ++w) {
-    const float sc = (S.mrg[w][0] == ninf()) ? 0.f : expf(S.mrg[w][0] - M);
-    O += accs[w * D + tid] * sc;
-    DD += S.mrg[w][1] * sc;
-  }
-  cs[8 + tid] = O;
-  if (tid == 0) {
-    float cn = 0.f;
-    double e2 = 0.0, s2 = 0.0;
-    for (int w = 0; w < PB_WARPS; ++w) {
-      cn = fmaxf(cn, S.mrg[w][2]);
-      e2 += S.mrgd[w][0];
-      s2 += S.mrgd[w][1];
-    }
-    cs[0] = M;
-    cs[1] = DD;
-    cs[2] = cn;
-    cs[3] = 0.f;
-    reinterpret_cast<double*>(cs + 4)[0] = e2;
-    reinterpret_cast<double*>(cs + 4)[1] = s2;
-  }
-}
-
-// =============================================================================
-// combine
-// =============================================================================
-__global__ void __launch_bounds__(128) k_combine(StepArgs a) {
-  const ckv_cache& c = a.c;
-  const ckv_step& st = a.st;
-  const ckv_policy& pol = a.pol;
-  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
-  const int nh = st.n_heads;
-  const size_t hu = (size_t)u * nh + h;
-  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
-  const int C = st.n_chunks;
-  const float* cs0 = st.chunk_state + hu * C * CKV_CHUNK_FLOATS;
-  const int pl = c.partial_len[u];
-  __shared__ int bad;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-
-  float M = (hs.lA > 0.f) ? hs.mA : ninf();
-  for (int k = 0; k < C; ++k) M = fmaxf(M, cs0[k * CKV_CHUNK_FLOATS]);
-  if (pl > 0) M = fmaxf(M, hs.mp);
-  float den = 0.f, num = 0.f;
-  if (hs.lA > 0.f) {
-    const float sc = expf(hs.mA - M);
-    den += hs.lA * sc;
-    num += hs.oA[tid] * sc;
-  }
-  float canary = 0.f;
-  double eF = 0.0, sF = 0.0;
-  for (int k = 0; k < C; ++k) {
-    const float* cs = cs0 + k * CKV_CHUNK_FLOATS;
-    if (cs[0] == ninf()) continue;
-    const float sc = expf(cs[0] - M);
-    den += cs[1] * sc;
-    num += cs[8 + tid] * sc;
-    canary = fmaxf(canary, cs[2]);
-    eF += reinterpret_cast<const double*>(cs + 4)[0];
-    sF += reinterpret_cast<const double*>(cs + 4)[1];
-  }
-  if (pl > 0) {
-    const float sc = expf(hs.mp - M);
-    den += hs.lp * sc;
-    num += hs.np_[tid] * sc;
-  }
-  const float out = num / den;
-  if (!isfinite(out) || !(den > 0.f)) atomicOr(&bad, 1);
-  st.out[hu * D + tid] = out;
-  __syncthreads();
-
-  if (tid == 0) {
-    ckv_cert& ct = st.cert[hu];
-    uint32_t fl = ct.flags;
-    const int kp = hs.kprime;
-    const int r = pol.ranking_depth;
-    const int32_t* order = st.order + hu * st.kcap;
-    const float* lm2 = st.lm2 + hu * st.kcap;
-    const double delta = (double)hs.delta;
-    if (pol.ranking_checks_enabled && kp > 0) {
-      if (kp < r) {
-        fl |= CKV_F_RANKING;
-      } else {
-        // top-r of the phase-2 log-masses (ties -> lower block index) vs the
-        // phase-1 order prefix (fallback.py:164-187, harness.py:231-250)
-        int picked[64];
-        float rth = 0.f;
-        bool same = true;
-        const int rr = min(r, 64);
-        for (int j = 0; j < rr; ++j) {
-          int best = -1;
-          float bv = 0.f;
-          int bb = 0x7fffffff;
-          for (int i = 0; i < kp; ++i) {
-            bool used = false;
-            for (int q = 0; q < j; ++q) used |= (picked[q] == i);
-            if (used) continue;
-            const float v = lm2[i];
-            const int bi = order[i];
-            if (best < 0 || v > bv || (v == bv && bi < bb)) {
-              best = i;
-              bv = v;
-              bb = bi;
-            }
-          }
-          picked[j] = best;
-          rth = bv;
-          if (order[j] != bb) same = false;
-        }
-        if (!same) fl |= CKV_F_RANKING;
-        if (hs.tailmax != ninf() && !((double)hs.tailmax + delta <= (double)rth)) fl |= CKV_F_BOUNDARY;
-      }
-    }
-    if (pol.canary_enabled && kp > 0) {
-      if (!((double)canary <= delta + pol.epsilon_guard)) fl |= CKV_F_CANARY;
-    }
-    if (bad) fl |= CKV_F_NUMERIC;
-    const double vmax = (double)c.v_max[u];
-    const double at = hs.alpha_hat;
-    const double denomE = at + hs.partial_mass + sF;
-    ct.delta_h = delta;
-    ct.est_tail_mass = at;
-    ct.v_max = vmax;
-    ct.e_key_tight = 2.0 * vmax * exp(2.0 * delta) * at * (exp(2.0 * delta) - 1.0);
-    // certifier.py:191-212 records both exponent modes; returned_e_key uses mode 3
-    ct.e_key_impl = 2.0 * vmax * exp(3.0 * delta) * at * (exp(2.0 * delta) - 1.0);
-    ct.e_val = (denomE > 0.0) ? (hs.e_tail + eF) / denomE : 0.0;
-    ct.canary_gap = (double)canary;
-    ct.flags = fl;
-    int kind = 0;
-    if (fl & (CKV_F_CANARY | CKV_F_NUMERIC)) kind = 2;
-    else if (fl & (CKV_F_RANKING | CKV_F_BOUNDARY)) kind = 1;
-    ct.returned_kind = kind;
   }
 }
 
@@ -1004,6 +643,7 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // launchers
 // =============================================================================
 extern int g_launches;
+cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, cudaStream_t);
 
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                           int host_max_blocks, cudaStream_t s) {
@@ -1014,8 +654,6 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(PassBSmem));
     attrs = true;
   }
   const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
@@ -1028,10 +666,9 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   k_select<<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
-  k_pass_b<<<dim3(st->n_chunks, st->n_heads, c->n_units), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
-  ++g_launches;
-  k_combine<<<dim3(st->n_heads, c->n_units), 128, 0, s>>>(a);
-  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_passb(c, pol, st, s);
   return cudaGetLastError();
 }
 

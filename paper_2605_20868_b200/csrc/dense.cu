@@ -9,7 +9,7 @@
 //                  the sequence; the four q-heads of a unit share each K/V read.
 //   k_dense_merge  merges the splits and overwrites the fast-path output of
 //                  every dense head.
-#include "common.cuh"
+#include "step.cuh"
 
 namespace ckv {
 
@@ -53,13 +53,20 @@ __global__ void k_resolve(DenseArgs a) {
 }
 
 struct DenseSmem {
-  float qh[H][D];
-  float s[DN_WARPS][B][H];
-  float mrg[DN_WARPS][H][2];
+  float qh[H * D];
+  float w[DN_WARPS][B][H];
+  float al[DN_WARPS][H];
 };
 
+// Exact attention over the full blocks of one split of a flagged unit; all
+// four q-heads share every K/V read.  Scores come from orig_block (FP16 keys
+// x hi/lo-split q' on the tensor cores, fp32 accumulate); the softmax and the
+// value accumulation run in fp32.  The partial block is added in k_dense_merge
+// from the state k_select already computed for it.
 __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   __shared__ DenseSmem S;
+  __shared__ float ow[DN_WARPS][H][D];
+  __shared__ float mw[DN_WARPS][H][2];
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int item = blockIdx.y, sp = blockIdx.x;
@@ -69,134 +76,103 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   const int nh = st.n_heads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = c.n_blocks[u];
-  const int pl = c.partial_len[u];
-  const int ntok = nb * B + pl;
-  const int t0 = sp * DN_TOK, t1 = min(ntok, t0 + DN_TOK);
+  const int b0 = sp * (DN_TOK / B), b1 = min(nb, b0 + DN_TOK / B);
   float* outp = st.dense_part + (((size_t)item * a.n_dsplit + sp) * H) * 132;
-  for (int i = tid; i < H * D; i += blockDim.x) {
-    const int h = i / D;
-    S.qh[h][i % D] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845)
-                              : 0.f;
-  }
-  __syncthreads();
-  if (t0 >= t1) {
+  if (b0 >= b1) {
     for (int i = tid; i < H * 132; i += blockDim.x) outp[i] = (i % 132 == 0) ? dninf() : 0.f;
     return;
   }
-  // Tier-2 must hold every full block we read (cache.py:138-142)
-  for (int b = t0 / B + tid; b < min(nb, (t1 + B - 1) / B); b += blockDim.x)
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    const int h = i / D;
+    S.qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845) : 0.f;
+  }
+  // Tier-2 must hold every block we read (cache.py:138-142)
+  for (int b = b0 + tid; b < b1; b += blockDim.x)
     if (!c.tier2_valid[(size_t)u * c.max_blocks + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
-
-  const size_t t2 = (size_t)u * c.max_blocks * B * D;
-  float m[H], l[H], o[H][4];
-#pragma unroll
-  for (int h = 0; h < H; ++h) {
-    m[h] = dninf();
-    l[h] = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[h][j] = 0.f;
-  }
-  const int tok = lane >> 1, hf = lane & 1;
-  for (int base = t0 + warp * B; base < t1; base += DN_WARPS * B) {
-    // scores: two lanes per token, 64 channels each, 4 heads
-    const int t = base + tok;
-    float s4[H] = {0.f, 0.f, 0.f, 0.f};
-    if (t < t1) {
-      const uint16_t* kp = (t < nb * B) ? c.tier2_k + t2 + (size_t)t * D
-                                        : c.partial_k + ((size_t)u * B + (t - nb * B)) * D;
-      const uint4* k4 = reinterpret_cast<const uint4*>(kp + hf * 64);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint4 w = k4[k];
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 kf = __half22float2(*reinterpret_cast<const __half2*>(&ww[j]));
-          const int ch = hf * 64 + k * 8 + 2 * j;
-#pragma unroll
-          for (int h = 0; h < H; ++h) s4[h] = fmaf(kf.x, S.qh[h][ch], fmaf(kf.y, S.qh[h][ch + 1], s4[h]));
-        }
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < H; ++h) s4[h] += __shfl_xor_sync(0xffffffffu, s4[h], 1);
-    if (hf == 0) {
-#pragma unroll
-      for (int h = 0; h < H; ++h) S.s[warp][tok][h] = (t < t1) ? s4[h] : dninf();
-    }
-    __syncwarp();
-    const int nvalid = min(B, t1 - base);
-    float sc[B][H];
-#pragma unroll
-    for (int i = 0; i < B; ++i)
-#pragma unroll
-      for (int h = 0; h < H; ++h) sc[i][h] = S.s[warp][i][h];
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      float mx = m[h];
-#pragma unroll
-      for (int i = 0; i < B; ++i) mx = fmaxf(mx, sc[i][h]);
-      const float al = (m[h] == dninf()) ? 0.f : expf(m[h] - mx);
-      l[h] *= al;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) o[h][j] *= al;
-      m[h] = mx;
-    }
-    // values: lane owns channels 4*lane .. 4*lane+3
-    for (int i = 0; i < nvalid; ++i) {
-      const int tt = base + i;
-      const uint16_t* vp = (tt < nb * B) ? c.tier2_v + t2 + (size_t)tt * D
-                                         : c.partial_v + ((size_t)u * B + (tt - nb * B)) * D;
-      const uint2 raw = *reinterpret_cast<const uint2*>(vp + lane * 4);
-      const float2 a0 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-      const float2 a1 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-#pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const float p = expf(sc[i][h] - m[h]);
-        l[h] += p;
-        o[h][0] = fmaf(p, a0.x, o[h][0]);
-        o[h][1] = fmaf(p, a0.y, o[h][1]);
-        o[h][2] = fmaf(p, a1.x, o[h][2]);
-        o[h][3] = fmaf(p, a1.y, o[h][3]);
-      }
-    }
-    __syncwarp();
-  }
-  // merge warps through shared memory (reuse S.s as scratch for o)
-  __shared__ float ow[DN_WARPS][H][D];
-  if (lane == 0) {
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      S.mrg[warp][h][0] = m[h];
-      S.mrg[warp][h][1] = l[h];
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < H; ++h)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) ow[warp][h][lane * 4 + j] = o[h][j];
   __syncthreads();
-  for (int h = 0; h < H; ++h) {
+  QFrag16 f16;
+  load_qfrag16(f16, S.qh, lane);
+  const int h = lane & 3, t0 = lane >> 2;
+  const size_t ubk = (size_t)u * c.max_blocks;
+  float m_h = dninf(), l_h = 0.f;
+  float2 acc[H][2];
+#pragma unroll
+  for (int i = 0; i < H; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  for (int b = b0 + warp; b < b1; b += DN_WARPS) {
+    const float2 s = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
+    float bmx = fmaxf(s.x, s.y);
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 4));
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
+    const float m_new = fmaxf(m_h, bmx);
+    const float alpha = (m_h == dninf()) ? 0.f : expf(m_h - m_new);
+    m_h = m_new;
+    const float w0 = expf(s.x - m_h), w1 = expf(s.y - m_h);
+    l_h = l_h * alpha + w0 + w1;
+    S.w[warp][t0][h] = w0;
+    S.w[warp][t0 + 8][h] = w1;
+    if (lane < H) S.al[warp][lane] = alpha;
+    __syncwarp();
+    const float4 al4 = *reinterpret_cast<const float4*>(S.al[warp]);
+    const float alv[4] = {al4.x, al4.y, al4.z, al4.w};
+#pragma unroll
+    for (int hh = 0; hh < H; ++hh) {
+      acc[hh][0] = __fmul2_rn(acc[hh][0], make_float2(alv[hh], alv[hh]));
+      acc[hh][1] = __fmul2_rn(acc[hh][1], make_float2(alv[hh], alv[hh]));
+    }
+    const uint16_t* vp = c.tier2_v + (ubk + b) * B * D + lane * 4;
+#pragma unroll 4
+    for (int t = 0; t < B; ++t) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(vp + (size_t)t * D);
+      const float2 v01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+      const float2 v23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      const float4 w4 = *reinterpret_cast<const float4*>(S.w[warp][t]);
+      const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh) {
+        acc[hh][0] = __ffma2_rn(make_float2(wv[hh], wv[hh]), v01, acc[hh][0]);
+        acc[hh][1] = __ffma2_rn(make_float2(wv[hh], wv[hh]), v23, acc[hh][1]);
+      }
+    }
+    __syncwarp();
+  }
+  l_h += __shfl_xor_sync(0xffffffffu, l_h, 4);
+  l_h += __shfl_xor_sync(0xffffffffu, l_h, 8);
+  l_h += __shfl_xor_sync(0xffffffffu, l_h, 16);
+  if (lane < H) {
+    mw[warp][lane][0] = m_h;
+    mw[warp][lane][1] = l_h;
+  }
+#pragma unroll
+  for (int hh = 0; hh < H; ++hh) {
+    ow[warp][hh][lane * 4 + 0] = acc[hh][0].x;
+    ow[warp][hh][lane * 4 + 1] = acc[hh][0].y;
+    ow[warp][hh][lane * 4 + 2] = acc[hh][1].x;
+    ow[warp][hh][lane * 4 + 3] = acc[hh][1].y;
+  }
+  __syncthreads();
+  for (int hh = 0; hh < H; ++hh) {
     float M = dninf();
-    for (int w = 0; w < DN_WARPS; ++w) M = fmaxf(M, S.mrg[w][h][0]);
+    for (int w = 0; w < DN_WARPS; ++w) M = fmaxf(M, mw[w][hh][0]);
     float L = 0.f, O = 0.f;
     if (M != dninf()) {
       for (int w = 0; w < DN_WARPS; ++w) {
-        if (S.mrg[w][h][0] == dninf()) continue;
-        const float sc2 = expf(S.mrg[w][h][0] - M);
-        L += S.mrg[w][h][1] * sc2;
-        O += ow[w][h][tid] * sc2;
+        if (mw[w][hh][0] == dninf()) continue;
+        const float sc = expf(mw[w][hh][0] - M);
+        L += mw[w][hh][1] * sc;
+        O += ow[w][hh][tid] * sc;
       }
     }
     if (tid == 0) {
-      outp[h * 132 + 0] = M;
-      outp[h * 132 + 1] = L;
+      outp[hh * 132 + 0] = M;
+      outp[hh * 132 + 1] = L;
     }
-    outp[h * 132 + 4 + tid] = O;
+    outp[hh * 132 + 4 + tid] = O;
   }
 }
 
 __global__ void k_dense_merge(DenseArgs a) {
+  const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int item = blockIdx.x;
   if (item >= st.dense_list[0]) return;
@@ -204,10 +180,15 @@ __global__ void k_dense_merge(DenseArgs a) {
   const int u = e & 0xffffff, mask = (e >> 24) & 0xf;
   const int nh = st.n_heads;
   const int tid = threadIdx.x;
+  const int pl = c.partial_len[u];
   for (int h = 0; h < nh; ++h) {
     if (!((mask >> h) & 1)) continue;
+    const HeadState& hs =
+        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + h) * CKV_HEAD_FLOATS);
+    const float mp = hs.mp, lp = hs.lp;
+    const float* np_ = hs.np_;
     const float* p0 = st.dense_part + ((size_t)item * a.n_dsplit * H) * 132;
-    float M = dninf();
+    float M = (pl > 0) ? mp : dninf();
     for (int s = 0; s < a.n_dsplit; ++s) M = fmaxf(M, p0[(s * H + h) * 132]);
     float L = 0.f, O = 0.f;
     for (int s = 0; s < a.n_dsplit; ++s) {
@@ -217,6 +198,11 @@ __global__ void k_dense_merge(DenseArgs a) {
       L += p[1] * sc;
       O += p[4 + tid] * sc;
     }
+    if (pl > 0) {
+      const float sc = expf(mp - M);
+      L += lp * sc;
+      O += np_[tid] * sc;
+    }
     st.out[((size_t)u * nh + h) * D + tid] = O / L;
   }
 }
@@ -225,7 +211,7 @@ extern int g_launches;
 
 cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_tokens, cudaStream_t s) {
   DenseArgs a{*c, *st, st->rung4_group > 0 ? st->rung4_group : c->n_units, 0};
-  a.n_dsplit = (host_max_tokens + DN_TOK - 1) / DN_TOK;
+  a.n_dsplit = (host_max_tokens + DN_TOK - 1) / DN_TOK;  // full blocks only; partial via head state
   if (a.n_dsplit < 1) a.n_dsplit = 1;
   if (a.n_dsplit > st->n_dsplit_cap) a.n_dsplit = st->n_dsplit_cap;
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t), s);

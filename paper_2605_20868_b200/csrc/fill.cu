@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
     }
     kx[t] = half_bits_to_double(kb);
     sv[t][tid] = vb;
-    c.tier2_k[t2base + t * D + tid] = kb;
+    c.tier2_k[t2base + k2_offset(t, tid)] = kb;
     c.tier2_v[t2base + t * D + tid] = vb;
   }
 

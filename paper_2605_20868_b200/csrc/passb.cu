@@ -1,0 +1,477 @@
+// Pass B and combine.
+//
+//   k_union    per unit: the union over its q-heads of promoted (F_h) and
+//              value-promoted (V_h) blocks, ascending, with 4-bit head masks.
+//   k_pass_b   per unit over that union only: the block's quantized scores
+//              for all 4 heads (phase1_block, bit-identical to pass A), the
+//              original-key scores on the tensor cores (orig_block over the
+//              fragment-ordered FP16 Tier-2 keys), and per head the additive
+//              correction that turns pass A's speculative attend into the
+//              mask-gated Phase 2 of attention.py:251-282: for b in F_h
+//              add e^{s-m} v_new - e^{s'-m} v_hat, for b in V_h \ F_h add
+//              e^{s'-m} (v - v_hat).  Also the phase-2 log-mass of every
+//              promoted block (attention.py:283-296), the canary gap
+//              (fallback.py:190-199) and the F part of E_val.
+//   k_combine  per (unit, head): merge, output, ranking / boundary / canary
+//              monitors (harness.py:231-260), E_key / E_val (certifier.py:135-212).
+#include "step.cuh"
+
+namespace ckv {
+
+constexpr int UN_THREADS = 512;
+
+__global__ void __launch_bounds__(UN_THREADS) k_union(StepArgs a) {
+  extern __shared__ __align__(16) uint32_t ub[];
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const int u = blockIdx.x, tid = threadIdx.x;
+  const int nh = st.n_heads;
+  const int nb = c.n_blocks[u];
+  const int W = (c.max_blocks + 31) / 32;
+  uint32_t* fb = ub;           // [H][W]
+  uint32_t* vb = ub + H * W;   // [H][W]
+  __shared__ int ws[32];
+  __shared__ int tot;
+  for (int i = tid; i < 2 * H * W; i += UN_THREADS) ub[i] = 0u;
+  __syncthreads();
+  for (int h = 0; h < nh; ++h) {
+    const size_t hu = (size_t)u * nh + h;
+    const int kp = st.cert[hu].k_star;
+    const int nv = st.cert[hu].n_value_promoted;
+    const int32_t* ord = st.order + hu * st.kcap;
+    const int32_t* vl = st.vlist + hu * c.max_blocks;
+    for (int i = tid; i < kp; i += UN_THREADS) atomicOr(&fb[h * W + (ord[i] >> 5)], 1u << (ord[i] & 31));
+    for (int i = tid; i < nv; i += UN_THREADS) atomicOr(&vb[h * W + (vl[i] >> 5)], 1u << (vl[i] & 31));
+  }
+  __syncthreads();
+  const int per = (nb + UN_THREADS - 1) / UN_THREADS;
+  const int lo = tid * per, hi = min(nb, lo + per);
+  int cnt = 0;
+  for (int b = lo; b < hi; ++b) {
+    uint32_t any = 0;
+    for (int h = 0; h < nh; ++h) any |= (fb[h * W + (b >> 5)] | vb[h * W + (b >> 5)]) >> (b & 31);
+    cnt += any & 1u;
+  }
+  // block exclusive scan
+  const int lane = tid & 31, warp = tid >> 5;
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < UN_THREADS / 32) ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < UN_THREADS / 32) ws[lane] = w;
+    if (lane == UN_THREADS / 32 - 1) tot = w;
+  }
+  __syncthreads();
+  int pos = ((warp > 0) ? ws[warp - 1] : 0) + x - cnt;
+  int32_t* work = st.work + (size_t)u * st.wcap;
+  for (int b = lo; b < hi; ++b) {
+    uint32_t fm = 0, vm = 0;
+    for (int h = 0; h < nh; ++h) {
+      fm |= ((fb[h * W + (b >> 5)] >> (b & 31)) & 1u) << h;
+      vm |= ((vb[h * W + (b >> 5)] >> (b & 31)) & 1u) << h;
+    }
+    if (fm | vm) work[pos++] = b | (int)(fm << 24) | (int)(vm << 28);
+  }
+  if (tid == 0) st.n_work[u] = tot;
+}
+
+// -----------------------------------------------------------------------------
+constexpr int PB_WARPS = 4;
+constexpr int PB_IPC = 32;  // work items per chunk
+
+struct PassBSmem {
+  uint8_t rec[PB_WARPS][2][REC];
+  uint64_t bar[PB_WARPS][2];
+  float qh[H * D];
+  float wn[PB_WARPS][B][H];
+  float wq[PB_WARPS][B][H];
+  float al[PB_WARPS][H];
+};
+
+__global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const int ck = blockIdx.x, u = blockIdx.y;
+  const int C = gridDim.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nh = st.n_heads;
+  const int nwork = st.n_work[u];
+  float* cs = st.chunk_state + ((size_t)u * C + ck) * H * CKV_CHUNK_FLOATS;
+  if (ck * PB_IPC >= nwork) {
+    if (tid < H) cs[tid * CKV_CHUNK_FLOATS] = ninf();
+    return;
+  }
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    const int hh = i / D;
+    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
+                        : 0.f;
+  }
+  if (tid == 0) {
+    for (int w = 0; w < PB_WARPS; ++w) {
+      mbar_init(&S.bar[w][0], 1);
+      mbar_init(&S.bar[w][1], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  QFrag f;
+  load_qfrag(f, S.qh, lane);
+  QFrag16 f16;
+  load_qfrag16(f16, S.qh, lane);
+
+  const int h = lane & 3;  // the head this lane's scores belong to
+  const HeadState* hs0 = reinterpret_cast<const HeadState*>(st.head_state + (size_t)u * nh * CKV_HEAD_FLOATS);
+  const int hq = (h < nh) ? h : 0;
+  const double lse = hs0[hq].lse;
+  float m_h = hs0[hq].mA;
+  if (m_h == ninf()) m_h = -1e30f;
+  float dden = 0.f, canary = 0.f;
+  double eF = 0.0, sF = 0.0;
+  float2 acc[H][2];
+#pragma unroll
+  for (int i = 0; i < H; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+
+  const size_t ubk = (size_t)u * c.max_blocks;
+  const int32_t* work = st.work + (size_t)u * st.wcap;
+  const float* eta = c.eta + ubk;
+  float* lm2 = st.lm2 + ((size_t)u * nh + hq) * c.max_blocks;
+  const int g = lane >> 2;
+  const int t0 = lane >> 2;
+
+  // this warp's item sequence: chunks ck, ck+C, ...; items base+warp, +4, ...
+  auto item_at = [&](int k) -> int {  // k-th item of this warp, or -1
+    const int per_chunk = (PB_IPC + PB_WARPS - 1 - warp) / PB_WARPS;
+    const int chunk = k / per_chunk, within = k % per_chunk;
+    const int idx = (ck + chunk * C) * PB_IPC + warp + within * PB_WARPS;
+    const int cend = min(nwork, (ck + chunk * C) * PB_IPC + PB_IPC);
+    return (idx < cend) ? idx : -1;
+  };
+  const uint8_t* t1base = c.tier1 + ubk * REC;
+  int cur = item_at(0);
+  if (lane == 0 && cur >= 0) {
+    const int b = work[cur] & 0xffffff;
+    mbar_expect_tx(&S.bar[warp][0], REC);
+    bulk_g2s(S.rec[warp][0], t1base + (size_t)b * REC, REC, &S.bar[warp][0]);
+  }
+  for (int k = 0; cur >= 0; ++k) {
+    const int stg = k & 1;
+    const int nxt = item_at(k + 1);
+    if (lane == 0 && nxt >= 0) {
+      const int b2 = work[nxt] & 0xffffff;
+      fence_proxy_async();
+      mbar_expect_tx(&S.bar[warp][stg ^ 1], REC);
+      bulk_g2s(S.rec[warp][stg ^ 1], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg ^ 1]);
+    }
+    const int e = work[cur];
+    const int b = e & 0xffffff;
+    const uint32_t fm = ((uint32_t)e >> 24) & 0xfu, vm = ((uint32_t)e >> 28) & 0xfu;
+    const bool inF = (fm >> h) & 1u, inV = (vm >> h) & 1u;
+    if ((fm | vm) && lane == 0 && !c.tier2_valid[ubk + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
+    const float smax = c.kscale_max[ubk + b];
+    mbar_wait(&S.bar[warp][stg], (uint32_t)(k >> 1) & 1u);
+    const uint8_t* rec = S.rec[warp][stg];
+
+    const BlockScores r = phase1_block(f, rec, smax, lane);
+    float sn0 = r.s0, sn1 = r.s1;
+    if (fm) {
+      const float2 so = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
+      if (inF) {
+        sn0 = so.x;
+        sn1 = so.y;
+      }
+    }
+    // per-head frame, weights, phase-2 block log-mass and canary
+    float bmx = fmaxf(sn0, sn1);
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 4));
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
+    bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 16));
+    const float m_new = fmaxf(m_h, bmx);
+    const float alpha = fast_exp(m_h - m_new);
+    m_h = m_new;
+    const float wn0 = fast_exp(sn0 - m_h), wn1 = fast_exp(sn1 - m_h);
+    const float wq0 = fast_exp(r.s0 - m_h), wq1 = fast_exp(r.s1 - m_h);
+    dden = dden * alpha + (inF ? (wn0 - wq0) + (wn1 - wq1) : 0.f);
+    if (fm) {
+      float es = fast_exp(sn0 - bmx) + fast_exp(sn1 - bmx);
+      float gap = fmaxf(fabsf(sn0 - r.s0), fabsf(sn1 - r.s1));
+      es += __shfl_xor_sync(0xffffffffu, es, 4);
+      es += __shfl_xor_sync(0xffffffffu, es, 8);
+      es += __shfl_xor_sync(0xffffffffu, es, 16);
+      gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 4));
+      gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 8));
+      gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 16));
+      if (inF) {
+        const float lb = bmx + __logf(es);
+        canary = fmaxf(canary, gap);
+        if (lane < H && h < nh) {
+          lm2[b] = lb;
+          const double rb = exp((double)lb - lse);
+          sF += rb;
+          if (!inV) eF += rb * (double)eta[b];
+        }
+      }
+    }
+    S.wn[warp][t0][h] = wn0;
+    S.wn[warp][t0 + 8][h] = wn1;
+    S.wq[warp][t0][h] = wq0;
+    S.wq[warp][t0 + 8][h] = wq1;
+    if (lane < H) S.al[warp][lane] = alpha;
+    __syncwarp();
+    {
+      const float4 al4 = *reinterpret_cast<const float4*>(S.al[warp]);
+      const float alv[4] = {al4.x, al4.y, al4.z, al4.w};
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh) {
+        acc[hh][0] = __fmul2_rn(acc[hh][0], make_float2(alv[hh], alv[hh]));
+        acc[hh][1] = __fmul2_rn(acc[hh][1], make_float2(alv[hh], alv[hh]));
+      }
+    }
+    // values: lane owns channels 4*lane .. 4*lane+3
+    const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+    const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+    const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(rec + OFF_VMETA + g * 64);
+    const uint16_t* vorig = c.tier2_v + (ubk + b) * B * D + lane * 4;
+#pragma unroll 4
+    for (int t = 0; t < B; ++t) {
+      const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
+      const uint32_t mm = vmeta[t];
+      const float2 sof = __half22float2(*reinterpret_cast<const __half2*>(&mm));
+      const float op = fmaf(-16.f, sof.x, sof.y);
+      float fbv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        fbv[j] = __uint_as_float(((cw << (19 - 4 * j)) & 0x00780000u) | 0x41800000u);
+      const float2 vq01 = __ffma2_rn(make_float2(fbv[0], fbv[1]), make_float2(sof.x, sof.x),
+                                     make_float2(op, op));
+      const float2 vq23 = __ffma2_rn(make_float2(fbv[2], fbv[3]), make_float2(sof.x, sof.x),
+                                     make_float2(op, op));
+      float2 vo01 = vq01, vo23 = vq23;
+      if (vm) {
+        const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
+        vo01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+        vo23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+      }
+      const float4 wn4 = *reinterpret_cast<const float4*>(S.wn[warp][t]);
+      const float4 wq4 = *reinterpret_cast<const float4*>(S.wq[warp][t]);
+      const float wnv[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
+      const float wqv[4] = {wq4.x, wq4.y, wq4.z, wq4.w};
+#pragma unroll
+      for (int hh = 0; hh < H; ++hh) {
+        const bool F = (fm >> hh) & 1u, V = (vm >> hh) & 1u;
+        if (!(F || V)) continue;
+        const float2 n01 = V ? vo01 : vq01, n23 = V ? vo23 : vq23;
+        if (F) {
+          acc[hh][0] = __ffma2_rn(make_float2(wnv[hh], wnv[hh]), n01, acc[hh][0]);
+          acc[hh][1] = __ffma2_rn(make_float2(wnv[hh], wnv[hh]), n23, acc[hh][1]);
+          acc[hh][0] = __ffma2_rn(make_float2(-wqv[hh], -wqv[hh]), vq01, acc[hh][0]);
+          acc[hh][1] = __ffma2_rn(make_float2(-wqv[hh], -wqv[hh]), vq23, acc[hh][1]);
+        } else {
+          const float2 d01 = make_float2(vo01.x - vq01.x, vo01.y - vq01.y);
+          const float2 d23 = make_float2(vo23.x - vq23.x, vo23.y - vq23.y);
+          acc[hh][0] = __ffma2_rn(make_float2(wqv[hh], wqv[hh]), d01, acc[hh][0]);
+          acc[hh][1] = __ffma2_rn(make_float2(wqv[hh], wqv[hh]), d23, acc[hh][1]);
+        }
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+
+  // ---- reduce within the warp (per head), then across the 4 warps ----------
+  dden += __shfl_xor_sync(0xffffffffu, dden, 4);
+  dden += __shfl_xor_sync(0xffffffffu, dden, 8);
+  dden += __shfl_xor_sync(0xffffffffu, dden, 16);
+  canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 4));
+  canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 8));
+  canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 16));
+  __syncthreads();
+  float* accs = reinterpret_cast<float*>(S.rec);             // [warp][H][D]
+  float* mw = accs + PB_WARPS * H * D;                        // [warp][H][4]
+  double* dw = reinterpret_cast<double*>(mw + PB_WARPS * H * 4);  // [warp][H][2]
+#pragma unroll
+  for (int hh = 0; hh < H; ++hh) {
+    float* p = accs + (warp * H + hh) * D + lane * 4;
+    p[0] = acc[hh][0].x;
+    p[1] = acc[hh][0].y;
+    p[2] = acc[hh][1].x;
+    p[3] = acc[hh][1].y;
+  }
+  if (lane < H) {
+    mw[(warp * H + lane) * 4 + 0] = m_h;
+    mw[(warp * H + lane) * 4 + 1] = dden;
+    mw[(warp * H + lane) * 4 + 2] = canary;
+    dw[(warp * H + lane) * 2 + 0] = eF;
+    dw[(warp * H + lane) * 2 + 1] = sF;
+  }
+  __syncthreads();
+  for (int hh = 0; hh < H; ++hh) {
+    float M = ninf();
+    for (int w = 0; w < PB_WARPS; ++w) M = fmaxf(M, mw[(w * H + hh) * 4]);
+    float O = 0.f, DD = 0.f, CN = 0.f;
+    double E2 = 0.0, S2 = 0.0;
+    for (int w = 0; w < PB_WARPS; ++w) {
+      const float sc = expf(mw[(w * H + hh) * 4] - M);
+      O += accs[(w * H + hh) * D + tid] * sc;
+      DD += mw[(w * H + hh) * 4 + 1] * sc;
+      CN = fmaxf(CN, mw[(w * H + hh) * 4 + 2]);
+      E2 += dw[(w * H + hh) * 2];
+      S2 += dw[(w * H + hh) * 2 + 1];
+    }
+    float* o = cs + hh * CKV_CHUNK_FLOATS;
+    o[8 + tid] = O;
+    if (tid == 0) {
+      o[0] = M;
+      o[1] = DD;
+      o[2] = CN;
+      o[3] = 0.f;
+      reinterpret_cast<double*>(o + 4)[0] = E2;
+      reinterpret_cast<double*>(o + 4)[1] = S2;
+    }
+  }
+}
+
+// -----------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_combine(StepArgs a) {
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const ckv_policy& pol = a.pol;
+  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+  const int nh = st.n_heads;
+  const size_t hu = (size_t)u * nh + h;
+  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+  const int C = st.n_chunks;
+  const int pl = c.partial_len[u];
+  __shared__ int bad;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  auto chunk = [&](int k) -> const float* {
+    return st.chunk_state + (((size_t)u * C + k) * H + h) * CKV_CHUNK_FLOATS;
+  };
+  float M = (hs.lA > 0.f) ? hs.mA : ninf();
+  for (int k = 0; k < C; ++k) M = fmaxf(M, chunk(k)[0]);
+  if (pl > 0) M = fmaxf(M, hs.mp);
+  float den = 0.f, num = 0.f;
+  if (hs.lA > 0.f) {
+    const float sc = expf(hs.mA - M);
+    den += hs.lA * sc;
+    num += hs.oA[tid] * sc;
+  }
+  float canary = 0.f;
+  double eF = 0.0, sF = 0.0;
+  for (int k = 0; k < C; ++k) {
+    const float* cs = chunk(k);
+    if (cs[0] == ninf()) continue;
+    const float sc = expf(cs[0] - M);
+    den += cs[1] * sc;
+    num += cs[8 + tid] * sc;
+    canary = fmaxf(canary, cs[2]);
+    eF += reinterpret_cast<const double*>(cs + 4)[0];
+    sF += reinterpret_cast<const double*>(cs + 4)[1];
+  }
+  if (pl > 0) {
+    const float sc = expf(hs.mp - M);
+    den += hs.lp * sc;
+    num += hs.np_[tid] * sc;
+  }
+  const float out = num / den;
+  if (!isfinite(out) || !(den > 0.f)) atomicOr(&bad, 1);
+  st.out[hu * D + tid] = out;
+  __syncthreads();
+
+  if (tid == 0) {
+    ckv_cert& ct = st.cert[hu];
+    uint32_t fl = ct.flags;
+    const int kp = hs.kprime;
+    const int r = pol.ranking_depth;
+    const int32_t* order = st.order + hu * st.kcap;
+    const float* lm2 = st.lm2 + hu * c.max_blocks;
+    const double delta = (double)hs.delta;
+    if (pol.ranking_checks_enabled && kp > 0) {
+      if (kp < r) {
+        fl |= CKV_F_RANKING;
+      } else {
+        // top-r of the phase-2 log-masses (ties -> lower block index) against
+        // the phase-1 order prefix (fallback.py:164-187, harness.py:231-250)
+        int picked[64];
+        float rth = 0.f;
+        bool same = true;
+        const int rr = min(r, 64);
+        for (int j = 0; j < rr; ++j) {
+          int best = -1, bb = 0x7fffffff;
+          float bv = 0.f;
+          for (int i = 0; i < kp; ++i) {
+            const int bi = order[i];
+            bool used = false;
+            for (int q = 0; q < j; ++q) used |= (picked[q] == bi);
+            if (used) continue;
+            const float v = lm2[bi];
+            if (best < 0 || v > bv || (v == bv && bi < bb)) {
+              best = i;
+              bv = v;
+              bb = bi;
+            }
+          }
+          picked[j] = bb;
+          rth = bv;
+          if (order[j] != bb) same = false;
+        }
+        if (!same) fl |= CKV_F_RANKING;
+        if (hs.tailmax != ninf() && !((double)hs.tailmax + delta <= (double)rth)) fl |= CKV_F_BOUNDARY;
+      }
+    }
+    if (pol.canary_enabled && kp > 0) {
+      if (!((double)canary <= delta + pol.epsilon_guard)) fl |= CKV_F_CANARY;
+    }
+    if (bad) fl |= CKV_F_NUMERIC;
+    const double vmax = (double)c.v_max[u];
+    const double at = hs.alpha_hat;
+    const double denomE = at + hs.partial_mass + sF;
+    ct.delta_h = delta;
+    ct.est_tail_mass = at;
+    ct.v_max = vmax;
+    // certifier.py:191-212 records both exponent modes; returned_e_key uses mode 3
+    ct.e_key_tight = 2.0 * vmax * exp(2.0 * delta) * at * (exp(2.0 * delta) - 1.0);
+    ct.e_key_impl = 2.0 * vmax * exp(3.0 * delta) * at * (exp(2.0 * delta) - 1.0);
+    ct.e_val = (denomE > 0.0) ? (hs.e_tail + eF) / denomE : 0.0;
+    ct.canary_gap = (double)canary;
+    ct.flags = fl;
+    int kind = 0;
+    if (fl & (CKV_F_CANARY | CKV_F_NUMERIC)) kind = 2;
+    else if (fl & (CKV_F_RANKING | CKV_F_BOUNDARY)) kind = 1;
+    ct.returned_kind = kind;
+  }
+}
+
+extern int g_launches;
+
+cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st, cudaStream_t s) {
+  StepArgs a{*c, *st, *pol};
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
+    cudaFuncSetAttribute(k_union, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attrs = true;
+  }
+  const int W = (c->max_blocks + 31) / 32;
+  k_union<<<c->n_units, UN_THREADS, 2 * H * W * 4, s>>>(a);
+  k_pass_b<<<dim3(st->n_chunks, c->n_units), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  k_combine<<<dim3(st->n_heads, c->n_units), 128, 0, s>>>(a);
+  g_launches += 3;
+  return cudaGetLastError();
+}
+
+}  // namespace ckv

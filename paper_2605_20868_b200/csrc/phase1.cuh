@@ -135,4 +135,57 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// Original-key scores of a 16-token block for the four q-heads on the tensor
+// cores: A = the block's FP16 keys (fragment order, exact), B = q' split into
+// fp16 hi + lo (scaled by 2^(14-eQ) into fp16 range), fp32 accumulation.
+// Column n = 2h + part, so accumulator lane l owns head l%4 for tokens l/4,
+// l/4+8 -- the same layout as phase1_block.
+struct QFrag16 {
+  uint32_t b[8][2];
+  float unscale;  // 2^(eQ - 14) for head lane%4
+};
+
+__device__ inline void load_qfrag16(QFrag16& f, const float* qh, int lane) {
+  const int hb = lane >> 3, part = (lane >> 2) & 1;
+  int eq_b = 0, eq_l = 0;
+#pragma unroll
+  for (int h = 0; h < H; ++h) {
+    float m = 0.f;
+    for (int c = lane; c < D; c += 32) m = fmaxf(m, fabsf(qh[h * D + c]));
+    m = warp_max(m);
+    const int e = (m > 0.f) ? (ilogbf(m) + 1) : 0;
+    if (h == (lane & 3)) eq_l = e;
+    if (h == hb) eq_b = e;
+  }
+  const float sc = pow2f(14 - eq_b);
+  f.unscale = pow2f(eq_l - 14);
+#pragma unroll
+  for (int kt = 0; kt < 8; ++kt) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int c = kt * 16 + (lane & 3) * 2 + 8 * p;
+      const float x0 = qh[hb * D + c] * sc, x1 = qh[hb * D + c + 1] * sc;
+      __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+      if (part) {
+        h0 = __float2half_rn(x0 - __half2float(h0));
+        h1 = __float2half_rn(x1 - __half2float(h1));
+      }
+      __half2 v = __halves2half2(h0, h1);
+      f.b[kt][p] = *reinterpret_cast<uint32_t*>(&v);
+    }
+  }
+}
+
+// kf: the block's Tier-2 keys (4 KB, fragment order) in global memory.
+__device__ __forceinline__ float2 orig_block(const QFrag16& f, const uint4* kf, int lane) {
+  float d[4] = {0.f, 0.f, 0.f, 0.f};
+  uint4 a[8];
+#pragma unroll
+  for (int kt = 0; kt < 8; ++kt) a[kt] = kf[kt * 32 + lane];
+#pragma unroll
+  for (int kt = 0; kt < 8; ++kt) mma_f16(d, a[kt], f.b[kt][0], f.b[kt][1]);
+  return make_float2((d[0] + d[1]) * f.unscale, (d[2] + d[3]) * f.unscale);
+}
+
 }  // namespace ckv

@@ -1,0 +1,41 @@
+// Device-side state shared by the decode-step kernels.
+#pragma once
+#include <cstddef>
+#include "phase1.cuh"
+
+namespace ckv {
+
+struct HeadState {
+  double lse;          // phase-1 log-sum-exp over full blocks + partial
+  double alpha_hat;    // estimated tail mass (non-promoted full blocks)
+  double e_tail;       // sum over b not in F u V of p_b eta_b
+  double partial_mass;
+  float mA, lA;        // merged pass-A softmax state
+  float delta;         // Delta_h
+  float tailmax;       // max phase-1 log-mass over the tail (-inf if empty)
+  float mp, lp;        // partial block state
+  int32_t kprime;      // |F| after rung 1
+  int32_t kstar0;      // K* before rung 1
+  int32_t n_v;
+  int32_t k_cov;
+  int32_t pad[2];
+  float oA[D];
+  float np_[D];
+};
+static_assert(sizeof(HeadState) <= CKV_HEAD_FLOATS * 4, "head state too large");
+
+
+struct StepArgs {
+  ckv_cache c;
+  ckv_step st;
+  ckv_policy pol;
+};
+
+__device__ __forceinline__ float ninf() { return __int_as_float(0xff800000); }
+
+__device__ __forceinline__ uint32_t okey(float x) {  // order-preserving float -> u32
+  uint32_t b = __float_as_uint(x);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+}  // namespace ckv

@@ -79,12 +79,12 @@ class CertifiedDecoder:
         self.split_state = torch.zeros((U, st.n_splits, 4, _lib.SPLIT_FLOATS),
                                        dtype=torch.float32, device=dev)
         self.order = torch.zeros((U, nh, st.kcap), dtype=torch.int32, device=dev)
-        self.work = torch.zeros((U, nh, st.wcap), dtype=torch.int32, device=dev)
-        self.n_work = torch.zeros((U, nh), dtype=torch.int32, device=dev)
+        self.work = torch.zeros((U, st.wcap), dtype=torch.int32, device=dev)
+        self.n_work = torch.zeros((U,), dtype=torch.int32, device=dev)
         self.vlist = torch.zeros((U, nh, NB), dtype=torch.int32, device=dev)
-        self.lm2 = torch.zeros((U, nh, st.kcap), dtype=torch.float32, device=dev)
+        self.lm2 = torch.zeros((U, nh, NB), dtype=torch.float32, device=dev)
         self.head_state = torch.zeros((U, nh, _lib.HEAD_FLOATS), dtype=torch.float32, device=dev)
-        self.chunk_state = torch.zeros((U, nh, st.n_chunks, _lib.CHUNK_FLOATS),
+        self.chunk_state = torch.zeros((U, st.n_chunks, 4, _lib.CHUNK_FLOATS),
                                        dtype=torch.float32, device=dev)
         self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
         self.dense_list = torch.zeros((U + 1,), dtype=torch.int32, device=dev)
