@@ -220,6 +220,9 @@ ckv_status ckv_fused_attend(const float* scores, const float* values, const int6
  * on this thread (for the bench's gpu_launches claim). */
 int32_t ckv_last_launches(void);
 
+/* Text of the last CUDA error that produced CKV_ECUDA on this thread. */
+const char* ckv_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

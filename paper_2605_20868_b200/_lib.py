@@ -99,6 +99,7 @@ def load():
         "ckv_fused_attend": (I32, [P, P, P, I32, I32, P, P, P]),
         "ckv_last_launches": (I32, []),
         "ckv_f64_to_f16": (I32, [P, P, ctypes.c_int64, P]),
+        "ckv_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -113,7 +114,7 @@ def exported_symbols():
     return ["ckv_version", "ckv_lru_words", "ckv_scratch_init", "ckv_plan", "ckv_append",
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
             "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
-            "ckv_f64_to_f16"]
+            "ckv_f64_to_f16", "ckv_last_error"]
 
 
 def check(code, what):
@@ -130,4 +131,7 @@ def check(code, what):
         raise PagingError(f"{what}: {name}")
     if code == 5:
         raise Tier2UnavailableError(f"{what}: {name}")
-    raise RuntimeError(f"{what}: {name}")
+    detail = ""
+    if code == 7 and _lib is not None:
+        detail = " (" + (_lib.ckv_last_error() or b"").decode() + ")"
+    raise RuntimeError(f"{what}: {name}{detail}")

@@ -61,7 +61,7 @@ class DeviceKVCache:
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.n_units = int(n_units)
-        self.max_blocks = max(1, -(-int(max_tokens) // B))
+        self.max_blocks = max(32, -(-int(max_tokens) // (B * 32)) * 32)  # multiple of 32 blocks
         self.tier2_location = tier2
         U, NB = self.n_units, self.max_blocks
         kw = dict(device=self.device)

@@ -1,4 +1,5 @@
 // extern "C" entry points of libcertkv_b200.so (declared in include/certkv_b200.h).
+#include <cstdio>
 #include "common.cuh"
 
 namespace ckv {
@@ -21,7 +22,12 @@ cudaError_t launch_fused_attend(const float*, const float*, const int64_t*, int,
                                 cudaStream_t);
 }  // namespace ckv
 
-static ckv_status st_of(cudaError_t e) { return e == cudaSuccess ? CKV_OK : CKV_ECUDA; }
+static thread_local char g_err[256] = "";
+static ckv_status st_of(cudaError_t e) {
+  if (e == cudaSuccess) return CKV_OK;
+  snprintf(g_err, sizeof(g_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+  return CKV_ECUDA;
+}
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static bool cache_ok(const ckv_cache* c) {
@@ -55,6 +61,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
                     ckv_step* st) {
   if (!pol || !st || n_units <= 0 || max_blocks <= 0 || n_heads < 1 || n_heads > CKV_MAX_QHEADS)
     return CKV_EINVAL;
+  if (max_blocks > 512 * 64) return CKV_EINVAL;  /* selection holds <= 32768 blocks per unit */
   if (pol->k_max < 0 || pol->k_min < 0 || pol->k_max < pol->k_min || pol->k_max > 511 ||
       pol->ranking_depth < 1 || pol->ranking_depth > 64)
     return CKV_EINVAL;
@@ -94,14 +101,14 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
   if (host_max_blocks < 0 || host_max_blocks > c->max_blocks) return CKV_EINVAL;
   if (pol->greedy_value_budget >= 0.0) return CKV_EINVAL;  // greedy rung 2 not on device yet
   cudaError_t e = ckv::launch_decode(c, pol, st, host_max_blocks, S(stream));
-  if (e != cudaSuccess) return CKV_ECUDA;
+  if (e != cudaSuccess) return st_of(e);
   e = ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream));
-  if (e != cudaSuccess) return CKV_ECUDA;
+  if (e != cudaSuccess) return st_of(e);
   if (scratch) {
     if (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters)
       return CKV_EINVAL;
     e = ckv::launch_scratch(c, st, scratch, S(stream));
-    if (e != cudaSuccess) return CKV_ECUDA;
+    if (e != cudaSuccess) return st_of(e);
   }
   return CKV_OK;
 }
@@ -148,5 +155,7 @@ ckv_status ckv_f64_to_f16(const double* x, uint16_t* y, int64_t n, void* stream)
 }
 
 int32_t ckv_last_launches(void) { return ckv::g_launches; }
+
+const char* ckv_last_error(void) { return g_err; }
 
 }  // extern "C"

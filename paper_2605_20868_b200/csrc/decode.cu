@@ -286,16 +286,17 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
 
 struct SelSmem {
   unsigned long long sortk[SEL_MAXSORT];
+  unsigned long long cand[SEL_MAXSORT];
   double cum[SEL_MAXSORT];
   float qv[D];
   float ps[B];
-  int hist[256];
   int wsum[32];
   int misc[16];
   double redd[40];
   float redf[40];
 };
 
+template <int KPT>
 __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
@@ -368,129 +369,107 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     }
   }
 
+  // ---- this thread's blocks [tid*KPT, tid*KPT+KPT): l'_b in registers ------------
+  const int base = tid * KPT;
+  float v[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; j += 4) {
+    if (base + j + 3 < nb && ((reinterpret_cast<uintptr_t>(lm + base + j) & 15u) == 0)) {
+      const float4 x = *reinterpret_cast<const float4*>(lm + base + j);
+      v[j] = x.x; v[j + 1] = x.y; v[j + 2] = x.z; v[j + 3] = x.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[j + q] = (base + j + q < nb) ? lm[base + j + q] : ninf();
+    }
+  }
+
   // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
   float lmax = lmp;
-  for (int b = tid; b < nb; b += SEL_THREADS) lmax = fmaxf(lmax, lm[b]);
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, v[j]);
   lmax = block_max_f(lmax, S.redf);
-  double se = 0.0;
-  for (int b = tid; b < nb; b += SEL_THREADS) se += exp((double)lm[b] - (double)lmax);
-  if (tid == 0 && pl > 0) se += exp((double)lmp - (double)lmax);
-  se = block_sum_d(se, S.redd);
+  float sef = 0.f;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) sef += (base + j < nb) ? expf(v[j] - lmax) : 0.f;
+  double se = block_sum_d((double)sef, S.redd);
+  if (pl > 0) se += exp((double)lmp - (double)lmax);
   const double lse = (double)lmax + log(se);
+  const float lsef = (float)lse;
   const double pmass = (pl > 0) ? exp((double)lmp - lse) : 0.0;
 
-  // ---- radix select of the top K_sel blocks by l' (ties -> lower index) -----------
+  // ---- top K_sel blocks by l' (ties -> lower index): bisection on the key ----------
   const int kwant = (pol.rung1_enabled ? 2 * pol.k_max : pol.k_max) + 1;
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
+  uint32_t kk[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) kk[j] = (base + j < nb) ? okey(v[j]) : 0u;
   int n_sorted = 0;
   if (ksel > 0) {
-    uint32_t prefix = 0u, mask = 0u;
-    int remaining = ksel;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = tid; i < 256; i += SEL_THREADS) S.hist[i] = 0;
-      __syncthreads();
-      for (int b = tid; b < nb; b += SEL_THREADS) {
-        const uint32_t k = okey(lm[b]);
-        if ((k & mask) == prefix) atomicAdd(&S.hist[(k >> shift) & 255u], 1);
-      }
-      __syncthreads();
-      if (warp == 0) {
-        // lane owns digits 255-8*lane .. 248-8*lane (descending)
-        int cnt[8], tot = 0;
+    // T = the largest key value with count(key >= T) >= ksel
+    uint32_t lo = 0u;
+    unsigned long long hi = 0x100000000ull;
+    while (hi - lo > 1ull) {
+      const uint32_t mid = (uint32_t)((lo + hi) >> 1);
+      int cnt = 0;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          cnt[j] = S.hist[255 - 8 * lane - j];
-          tot += cnt[j];
-        }
-        int incl = tot;
+      for (int j = 0; j < KPT; ++j) cnt += (kk[j] >= mid);
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) S.wsum[warp] = cnt;
+      __syncthreads();
+      int tot = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        int above = incl - tot;  // count in digits strictly greater than this lane's range
-        int found = -1, above_d = 0;
-        for (int j = 0; j < 8; ++j) {
-          if (found < 0 && above + cnt[j] >= remaining) {
-            found = 255 - 8 * lane - j;
-            above_d = above;
-          }
-          above += cnt[j];
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, found >= 0);
-        const int src = __ffs(bal) - 1;
-        const int dig = __shfl_sync(0xffffffffu, found, src);
-        const int abv = __shfl_sync(0xffffffffu, above_d, src);
-        if (lane == 0) {
-          S.misc[0] = dig;
-          S.misc[1] = abv;
-        }
-      }
+      for (int w = 0; w < SEL_THREADS / 32; ++w) tot += S.wsum[w];
       __syncthreads();
-      prefix |= (uint32_t)S.misc[0] << shift;
-      mask |= 255u << shift;
-      remaining -= S.misc[1];
-      __syncthreads();
+      if (tot >= ksel) lo = mid;
+      else hi = mid;
     }
-    // prefix = threshold key T; take all keys > T and the first `remaining` == T
-    const int per = (nb + SEL_THREADS - 1) / SEL_THREADS;
-    const int lo_i = tid * per, hi_i = min(nb, lo_i + per);
+    const uint32_t T = lo;
     int ngt = 0, neq = 0;
-    for (int b = lo_i; b < hi_i; ++b) {
-      const uint32_t k = okey(lm[b]);
-      ngt += (k > prefix);
-      neq += (k == prefix);
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      ngt += (kk[j] > T);
+      neq += (kk[j] == T && base + j < nb);
     }
     const int off_gt = block_excl_scan(ngt, S.wsum, &S.misc[2]);
     const int tot_gt = S.misc[2];
     const int off_eq = block_excl_scan(neq, S.wsum, &S.misc[3]);
+    const int need = ksel - tot_gt;
     int pg = off_gt, pe = off_eq;
-    for (int b = lo_i; b < hi_i; ++b) {
-      const uint32_t k = okey(lm[b]);
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const int b = base + j;
       const unsigned long long comp =
-          ((unsigned long long)k << 32) | (unsigned long long)(0xffffffffu - (uint32_t)b);
-      if (k > prefix) {
-        S.sortk[pg++] = comp;
-      } else if (k == prefix) {
-        if (pe < remaining) S.sortk[tot_gt + pe] = comp;
+          ((unsigned long long)kk[j] << 32) | (unsigned long long)(0xffffffffu - (uint32_t)b);
+      if (kk[j] > T) {
+        S.cand[pg++] = comp;
+      } else if (kk[j] == T && b < nb) {
+        if (pe < need) S.cand[tot_gt + pe] = comp;
         ++pe;
       }
     }
     n_sorted = ksel;
-    int P = 1;
-    while (P < n_sorted) P <<= 1;
-    for (int i = n_sorted + tid; i < P; i += SEL_THREADS) S.sortk[i] = 0ull;
     __syncthreads();
-    // bitonic sort, descending
-    for (int k = 2; k <= P; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = tid; i < P; i += SEL_THREADS) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const unsigned long long x = S.sortk[i], y = S.sortk[ixj];
-            const bool desc = ((i & k) == 0);
-            if (desc ? (x < y) : (x > y)) {
-              S.sortk[i] = y;
-              S.sortk[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
+    // rank sort (composite keys are distinct): position = #greater
+    for (int i = tid; i < n_sorted; i += SEL_THREADS) {
+      const unsigned long long x = S.cand[i];
+      int r = 0;
+      for (int j = 0; j < n_sorted; ++j) r += (S.cand[j] > x);
+      S.sortk[r] = x;
     }
+    __syncthreads();
   }
 
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
   for (int i = tid; i < n_sorted; i += SEL_THREADS) {
     const uint32_t k = (uint32_t)(S.sortk[i] >> 32);
     const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-    S.cum[i] = exp((double)__uint_as_float(bits) - lse);
+    S.cum[i] = (double)expf(__uint_as_float(bits) - lsef);
   }
   __syncthreads();
-  if (warp == 0) {  // sequential-order prefix sum in fp64 (one warp, chunked)
+  if (warp == 0) {  // prefix sum in fp64 along the mass order (one warp, chunked)
     double carry = pmass;
-    for (int base = 0; base < n_sorted; base += 32) {
-      const int i = base + lane;
+    for (int b0 = 0; b0 < n_sorted; b0 += 32) {
+      const int i = b0 + lane;
       double x = (i < n_sorted) ? S.cum[i] : 0.0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -501,14 +480,13 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
   }
+  if (tid == 0) S.misc[4] = -1;
+  __syncthreads();
+  for (int i = tid; i < n_sorted; i += SEL_THREADS)
+    if (S.cum[i] >= pol.tau_cov && (i == 0 || S.cum[i - 1] < pol.tau_cov)) S.misc[4] = i + 1;
   __syncthreads();
   if (tid == 0) {
-    int kcov = -1;
-    for (int i = 0; i < n_sorted; ++i)
-      if (S.cum[i] >= pol.tau_cov) {
-        kcov = i + 1;
-        break;
-      }
+    int kcov = S.misc[4];
     if (kcov < 0 && n_sorted == nb) kcov = nb;
     int kstar;
     if (nb == 0) {
@@ -534,36 +512,35 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   }
   __syncthreads();
 
-  // ---- tail mass, rung 2, E_val tail, work list (fallback.py:141-161, certifier.py:153-160)
+  // ---- tail mass, rung 2, E_val tail (fallback.py:141-161, certifier.py:153-160) ----
   const float* eta = c.eta + (size_t)u * c.max_blocks;
   const bool r2 = pol.rung2_enabled != 0;
   double at = 0.0, et = 0.0;
-  const int per = (nb + SEL_THREADS - 1) / SEL_THREADS;
-  const int lo_i = tid * per, hi_i = min(nb, lo_i + per);
-  int nv = 0, nvx = 0;
-  for (int b = lo_i; b < hi_i; ++b) {
-    const double pb = exp((double)lm[b] - lse);
+  int nv = 0;
+  uint32_t vbits = 0u;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const int b = base + j;
+    if (b >= nb) continue;
+    const double pb = (double)expf(v[j] - lsef);
     const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
     const double pe = pb * (double)eta[b];
     const bool inV = r2 && (pe > pol.v_tol);
     if (!inF) at += pb;
     if (!inF && !inV) et += pe;
     nv += inV;
-    nvx += (inV && !inF);
+    vbits |= (uint32_t)inV << j;
   }
   at = block_sum_d(at, S.redd);
   et = block_sum_d(et, S.redd);
   const int vo = block_excl_scan(nv, S.wsum, &S.misc[7]);
   const int n_v = S.misc[7];
-  (void)nvx;
   {
     int32_t* vlist = st.vlist + hu * c.max_blocks;
     int pv = vo;
-    for (int b = lo_i; b < hi_i; ++b) {
-      const double pb = exp((double)lm[b] - lse);
-      const bool inV = r2 && (pb * (double)eta[b] > pol.v_tol);
-      if (inV) vlist[pv++] = b;
-    }
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+      if ((vbits >> j) & 1u) vlist[pv++] = base + j;
   }
   if (tid == 0) {
     hs.lse = lse;
@@ -653,7 +630,8 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
   const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
@@ -664,7 +642,10 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   }
   if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
-  k_select<<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+  if (c->max_blocks <= SEL_THREADS * 16)
+    k_select<16><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+  else
+    k_select<64><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -133,10 +133,11 @@ __global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
   load_qfrag16(f16, S.qh, lane);
 
   const int h = lane & 3;  // the head this lane's scores belong to
-  const HeadState* hs0 = reinterpret_cast<const HeadState*>(st.head_state + (size_t)u * nh * CKV_HEAD_FLOATS);
   const int hq = (h < nh) ? h : 0;
-  const double lse = hs0[hq].lse;
-  float m_h = hs0[hq].mA;
+  const HeadState& hsq =
+      *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + hq) * CKV_HEAD_FLOATS);
+  const double lse = hsq.lse;
+  float m_h = hsq.mA;
   if (m_h == ninf()) m_h = -1e30f;
   float dden = 0.f, canary = 0.f;
   double eF = 0.0, sF = 0.0;

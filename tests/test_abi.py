@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "certkv_b200.h")
 
 def _declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:ckv_status|int32_t)\s+(ckv_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:ckv_status|int32_t|const char\*)\s+(ckv_\w+)\s*\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
