@@ -260,6 +260,8 @@ def main():
     launches = {"n": 0}
     dense_heads = {"n": 0}
 
+    last = {}
+
     def one_step(i, timed_ev=None):
         if timed_ev is not None:
             dec.st.prof_begin = timed_ev[0].cuda_event
@@ -269,6 +271,7 @@ def main():
         dec.st.prof_end = None
         launches["n"] += lib.ckv_last_launches()
         dense_heads["n"] += int((res.kinds != 0).sum())
+        last["res"] = res
         exchange()
         cache.append(kpool[i], vpool[i], validate=False)
         launches["n"] += lib.ckv_last_launches()
@@ -377,6 +380,8 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_launch,
+        "k_star_mean": float(last["res"].cert["k_star"].mean()),
+        "promoted_union_blocks_per_unit": float(dec.n_work.float().mean().item()),
         "dense_heads_in_timed_region": n_dense,
         "clocks": clocks,
         "prefill_s": prefill_s,

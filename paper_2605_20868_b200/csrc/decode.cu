@@ -369,28 +369,28 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     }
   }
 
-  // ---- this thread's blocks [tid*KPT, tid*KPT+KPT): l'_b in registers ------------
+  // ---- this thread's blocks [tid*KPT, tid*KPT+KPT): order keys of l'_b in registers
   const int base = tid * KPT;
-  float v[KPT];
+  uint32_t kk[KPT];
 #pragma unroll
   for (int j = 0; j < KPT; j += 4) {
     if (base + j + 3 < nb && ((reinterpret_cast<uintptr_t>(lm + base + j) & 15u) == 0)) {
       const float4 x = *reinterpret_cast<const float4*>(lm + base + j);
-      v[j] = x.x; v[j + 1] = x.y; v[j + 2] = x.z; v[j + 3] = x.w;
+      kk[j] = okey(x.x); kk[j + 1] = okey(x.y); kk[j + 2] = okey(x.z); kk[j + 3] = okey(x.w);
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[j + q] = (base + j + q < nb) ? lm[base + j + q] : ninf();
+      for (int q = 0; q < 4; ++q) kk[j + q] = (base + j + q < nb) ? okey(lm[base + j + q]) : 0u;
     }
   }
 
   // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
   float lmax = lmp;
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, v[j]);
+  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, (base + j < nb) ? ukey(kk[j]) : ninf());
   lmax = block_max_f(lmax, S.redf);
   float sef = 0.f;
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) sef += (base + j < nb) ? expf(v[j] - lmax) : 0.f;
+  for (int j = 0; j < KPT; ++j) sef += (base + j < nb) ? expf(ukey(kk[j]) - lmax) : 0.f;
   double se = block_sum_d((double)sef, S.redd);
   if (pl > 0) se += exp((double)lmp - (double)lmax);
   const double lse = (double)lmax + log(se);
@@ -400,9 +400,6 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   // ---- top K_sel blocks by l' (ties -> lower index): bisection on the key ----------
   const int kwant = (pol.rung1_enabled ? 2 * pol.k_max : pol.k_max) + 1;
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
-  uint32_t kk[KPT];
-#pragma unroll
-  for (int j = 0; j < KPT; ++j) kk[j] = (base + j < nb) ? okey(v[j]) : 0u;
   int n_sorted = 0;
   if (ksel > 0) {
     // T = the largest key value with count(key >= T) >= ksel
@@ -461,9 +458,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
 
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
   for (int i = tid; i < n_sorted; i += SEL_THREADS) {
-    const uint32_t k = (uint32_t)(S.sortk[i] >> 32);
-    const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-    S.cum[i] = (double)expf(__uint_as_float(bits) - lsef);
+    S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
   }
   __syncthreads();
   if (warp == 0) {  // prefix sum in fp64 along the mass order (one warp, chunked)
@@ -522,7 +517,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   for (int j = 0; j < KPT; ++j) {
     const int b = base + j;
     if (b >= nb) continue;
-    const double pb = (double)expf(v[j] - lsef);
+    const double pb = (double)expf(ukey(kk[j]) - lsef);
     const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
     const double pe = pb * (double)eta[b];
     const bool inV = r2 && (pe > pol.v_tol);
@@ -548,11 +543,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     hs.e_tail = et;
     hs.partial_mass = pmass;
     float tm = ninf();
-    if (kp < nb && kp < n_sorted) {
-      const uint32_t k = (uint32_t)(S.sortk[kp] >> 32);
-      const uint32_t bits = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
-      tm = __uint_as_float(bits);
-    }
+    if (kp < nb && kp < n_sorted) tm = ukey((uint32_t)(S.sortk[kp] >> 32));
     hs.tailmax = tm;
     hs.kprime = kp;
     hs.kstar0 = kstar;
@@ -631,6 +622,7 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
     cudaFuncSetAttribute(k_select<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
@@ -642,8 +634,11 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   }
   if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
-  if (c->max_blocks <= SEL_THREADS * 16)
+  const int nbh = host_max_blocks;  // selection only touches the filled blocks
+  if (nbh <= SEL_THREADS * 16)
     k_select<16><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+  else if (nbh <= SEL_THREADS * 32)
+    k_select<32><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   else
     k_select<64><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   ++g_launches;

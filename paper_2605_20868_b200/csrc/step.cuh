@@ -38,4 +38,8 @@ __device__ __forceinline__ uint32_t okey(float x) {  // order-preserving float -
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+__device__ __forceinline__ float ukey(uint32_t k) {  // inverse of okey
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
 }  // namespace ckv

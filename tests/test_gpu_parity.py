@@ -107,7 +107,8 @@ def test_nonfinite_append_is_rejected_without_mutation(ck):
     assert cache.num_tokens == 5 and int(cache.n_blocks_t.sum()) == 0
     assert cache.partial_len_t.cpu().tolist() == [5, 5]
     with pytest.raises(ValueError, match="capacity"):
-        cache.append(torch.zeros((2, 80, 128), device="cuda"), torch.zeros((2, 80, 128), device="cuda"))
+        big = torch.zeros((2, cache.max_blocks * 16 + 16, 128), device="cuda")
+        cache.append(big, big)
 
 
 # ---- plugin kernels -----------------------------------------------------------
