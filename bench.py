@@ -187,7 +187,7 @@ def main():
             ncpu = len(os.sched_getaffinity(0))
         except Exception:
             ncpu = os.cpu_count() or 1
-        workers = max(1, min(ncpu, 16))
+        workers = max(1, min(ncpu, 32))
         rate, dt, build_s = cpu_reference(args, total_units, K, W, workers)
         line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
                 "warmup": W, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
@@ -213,11 +213,10 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
-    # KV-head sharding: units are kv-major (u = kv * layers*batch + layer*batch + seq)
+    # KV-head sharding: units are kv-major (sharding.unit_index); rank r owns whole KV heads
     if args.kv_heads % world:
         raise SystemExit("kv_heads must be divisible by the number of GPUs")
-    per = total_units // world
-    U = per
+    U = total_units // world
     max_tokens = args.ctx + 2 * (K + W) + 32
     cache = ck.DeviceKVCache(U, max_tokens, device=dev, tier2=args.tier2)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
@@ -234,7 +233,6 @@ def main():
     pol = ck.PolicyConfig(exploration_rate=0.0)
     cap = cache.max_blocks if args.scratch < 0 else args.scratch
     scratch = ck.ScratchCache(cap) if args.scratch != 0 else None
-    group = args.kv_heads // world  # units sharing a layer's step-wide rung 4 (local part)
     dec = ck.CertifiedDecoder(cache, pol, n_heads=args.q_per_kv, scratch=scratch,
                               rung4_group=None)
     nq = W + K
@@ -246,16 +244,18 @@ def main():
     for a, b in ev_a:  # torch creates the CUDA event lazily: force it before handing it over
         a.record()
         b.record()
-    gather_bytes = U * args.q_per_kv * (128 * 4 + 88)
-    gbuf = torch.empty(gather_bytes * world, dtype=torch.uint8, device=dev)
+    from paper_2605_20868_b200 import sharding
+    my_units = sharding.shard_units(args.layers, args.kv_heads, args.batch, world, rank)
+    my_layers = sharding.layer_of_units(my_units, args.layers, args.batch)
 
-    def exchange():
+    def exchange(res):
         if world == 1:
             return
-        # outputs + certificates -> every rank (the bound report), one NCCL call
-        local_buf = torch.cat([dec.out.view(torch.uint8).reshape(-1),
-                               dec.cert_buf.reshape(-1)])
-        dist.all_gather_into_tensor(gbuf, local_buf)
+        # the bound report: outputs + certificates of every rank (one NCCL all-gather),
+        # and the per-layer Rung-4 flag (MAX all-reduce)
+        sharding.gather_bound_report(dec.out, dec.cert_buf)
+        r4 = (res.cert["flags"] & (_lib.F_CANARY | _lib.F_NUMERIC)).any(axis=1)
+        sharding.rung4_layers(r4, my_layers, args.layers, device=dev)
 
     launches = {"n": 0}
     dense_heads = {"n": 0}
@@ -272,7 +272,7 @@ def main():
         launches["n"] += lib.ckv_last_launches()
         dense_heads["n"] += int((res.kinds != 0).sum())
         last["res"] = res
-        exchange()
+        exchange(res)
         cache.append(kpool[i], vpool[i], validate=False)
         launches["n"] += lib.ckv_last_launches()
         return res
@@ -327,7 +327,7 @@ def main():
         e0 = time.perf_counter()
         for i in range(K):
             res = dec.step(qh[i].to(dev, non_blocking=True))
-            exchange()
+            exchange(res)
             oh.copy_(dec.out, non_blocking=True)
             cache.append(kh[i].to(dev, non_blocking=True), vh[i].to(dev, non_blocking=True))
         torch.cuda.synchronize()

@@ -26,7 +26,7 @@ namespace ckv {
 // pass A
 // =============================================================================
 constexpr int PA_WARPS = 4;
-constexpr int PA_STAGES = 3;
+constexpr int PA_STAGES = 2;
 
 struct PassASmem {
   uint8_t stage[PA_WARPS][PA_STAGES][REC];
@@ -36,7 +36,7 @@ struct PassASmem {
   float abuf[PA_WARPS][H];
 };
 
-__global__ void __launch_bounds__(PA_WARPS * 32) k_pass_a(StepArgs a) {
+__global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;

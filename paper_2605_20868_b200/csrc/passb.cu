@@ -225,10 +225,13 @@ __global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
         }
       }
     }
-    S.wn[warp][t0][h] = wn0;
-    S.wn[warp][t0 + 8][h] = wn1;
-    S.wq[warp][t0][h] = wq0;
-    S.wq[warp][t0 + 8][h] = wq1;
+    // branch-free correction coefficients: acc_h += a * v_orig + c * v_hat
+    //   F & V: a = wn, c = -wq   F only: a = 0, c = wn - wq
+    //   V only: a = wq, c = -wq  neither: a = c = 0
+    S.wn[warp][t0][h] = inV ? (inF ? wn0 : wq0) : 0.f;
+    S.wn[warp][t0 + 8][h] = inV ? (inF ? wn1 : wq1) : 0.f;
+    S.wq[warp][t0][h] = inV ? -wq0 : (inF ? wn0 - wq0 : 0.f);
+    S.wq[warp][t0 + 8][h] = inV ? -wq1 : (inF ? wn1 - wq1 : 0.f);
     if (lane < H) S.al[warp][lane] = alpha;
     __syncwarp();
     {
@@ -260,31 +263,23 @@ __global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
                                      make_float2(op, op));
       const float2 vq23 = __ffma2_rn(make_float2(fbv[2], fbv[3]), make_float2(sof.x, sof.x),
                                      make_float2(op, op));
-      float2 vo01 = vq01, vo23 = vq23;
-      if (vm) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
-        vo01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-        vo23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-      }
-      const float4 wn4 = *reinterpret_cast<const float4*>(S.wn[warp][t]);
-      const float4 wq4 = *reinterpret_cast<const float4*>(S.wq[warp][t]);
-      const float wnv[4] = {wn4.x, wn4.y, wn4.z, wn4.w};
-      const float wqv[4] = {wq4.x, wq4.y, wq4.z, wq4.w};
+      const float4 a4 = *reinterpret_cast<const float4*>(S.wn[warp][t]);
+      const float4 c4 = *reinterpret_cast<const float4*>(S.wq[warp][t]);
+      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+      const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
       for (int hh = 0; hh < H; ++hh) {
-        const bool F = (fm >> hh) & 1u, V = (vm >> hh) & 1u;
-        if (!(F || V)) continue;
-        const float2 n01 = V ? vo01 : vq01, n23 = V ? vo23 : vq23;
-        if (F) {
-          acc[hh][0] = __ffma2_rn(make_float2(wnv[hh], wnv[hh]), n01, acc[hh][0]);
-          acc[hh][1] = __ffma2_rn(make_float2(wnv[hh], wnv[hh]), n23, acc[hh][1]);
-          acc[hh][0] = __ffma2_rn(make_float2(-wqv[hh], -wqv[hh]), vq01, acc[hh][0]);
-          acc[hh][1] = __ffma2_rn(make_float2(-wqv[hh], -wqv[hh]), vq23, acc[hh][1]);
-        } else {
-          const float2 d01 = make_float2(vo01.x - vq01.x, vo01.y - vq01.y);
-          const float2 d23 = make_float2(vo23.x - vq23.x, vo23.y - vq23.y);
-          acc[hh][0] = __ffma2_rn(make_float2(wqv[hh], wqv[hh]), d01, acc[hh][0]);
-          acc[hh][1] = __ffma2_rn(make_float2(wqv[hh], wqv[hh]), d23, acc[hh][1]);
+        acc[hh][0] = __ffma2_rn(make_float2(cv[hh], cv[hh]), vq01, acc[hh][0]);
+        acc[hh][1] = __ffma2_rn(make_float2(cv[hh], cv[hh]), vq23, acc[hh][1]);
+      }
+      if (vm) {  // warp-uniform: some head of this block is value-promoted
+        const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
+        const float2 vo01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+        const float2 vo23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+#pragma unroll
+        for (int hh = 0; hh < H; ++hh) {
+          acc[hh][0] = __ffma2_rn(make_float2(av[hh], av[hh]), vo01, acc[hh][0]);
+          acc[hh][1] = __ffma2_rn(make_float2(av[hh], av[hh]), vo23, acc[hh][1]);
         }
       }
     }

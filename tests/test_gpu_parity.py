@@ -312,3 +312,19 @@ def test_output_soundness_large(ck):
             err = float(torch.linalg.norm(res.out[u, h].double() - ref[h]))
             c = res.cert[u, h]
             assert err <= c["e_key_tight"] + c["e_val"] + 1e-5, (u, h, err)
+
+
+def test_host_tier2_matches_device_tier2(ck):
+    """Tier-2 in pinned host RAM (zero-copy reads of promoted originals) gives
+    the same step as Tier-2 in HBM."""
+    cfg = ck.WorkloadConfig(kind="sink", n_tokens=3000, head_dim=128, query_heads=8, kv_heads=2,
+                            steps=2, seed=4)
+    pol = ck.PolicyConfig(exploration_rate=0.0, v_tol=0.01)
+    outs = []
+    for where in ("device", "host"):
+        wl = ck.generate_workload(cfg, tier2=where)
+        r = ck.run_workload(wl, pol, 64, 64, keep_outputs=True)
+        outs.append((r.outputs, r.step_records))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(a, b)
+    assert outs[0][1] == outs[1][1]
