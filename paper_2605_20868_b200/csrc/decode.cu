@@ -291,6 +291,7 @@ struct SelSmem {
   float qv[D];
   float ps[B];
   int wsum[32];
+  int wsum2[32];
   int misc[16];
   double redd[40];
   float redf[40];
@@ -402,24 +403,49 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
   int n_sorted = 0;
   if (ksel > 0) {
-    // T = the largest key value with count(key >= T) >= ksel
-    uint32_t lo = 0u;
-    unsigned long long hi = 0x100000000ull;
+    // T = the largest key value with count(key >= T) >= ksel; bisection over
+    // [min key, max key] with one barrier per step (double-buffered partials)
+    uint32_t kmn = 0xffffffffu, kmx = 0u;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (base + j < nb) {
+        kmn = min(kmn, kk[j]);
+        kmx = max(kmx, kk[j]);
+      }
+    }
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (lane == 0) {
+      S.wsum[warp] = (int)kmn;
+      S.wsum2[warp] = (int)kmx;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < SEL_THREADS / 32; ++w) {
+      kmn = min(kmn, (uint32_t)S.wsum[w]);
+      kmx = max(kmx, (uint32_t)S.wsum2[w]);
+    }
+    __syncthreads();
+    uint32_t lo = kmn;                                   // count(key >= kmn) = nb >= ksel
+    unsigned long long hi = (unsigned long long)kmx + 1; // count(key >= kmx+1) = 0 < ksel
+    int par = 0;
     while (hi - lo > 1ull) {
       const uint32_t mid = (uint32_t)((lo + hi) >> 1);
       int cnt = 0;
 #pragma unroll
       for (int j = 0; j < KPT; ++j) cnt += (kk[j] >= mid);
       cnt = __reduce_add_sync(0xffffffffu, cnt);
-      if (lane == 0) S.wsum[warp] = cnt;
+      int* buf = par ? S.wsum2 : S.wsum;
+      if (lane == 0) buf[warp] = cnt;
       __syncthreads();
       int tot = 0;
 #pragma unroll
-      for (int w = 0; w < SEL_THREADS / 32; ++w) tot += S.wsum[w];
-      __syncthreads();
+      for (int w = 0; w < SEL_THREADS / 32; ++w) tot += buf[w];
+      par ^= 1;
       if (tot >= ksel) lo = mid;
       else hi = mid;
     }
+    __syncthreads();
     const uint32_t T = lo;
     int ngt = 0, neq = 0;
 #pragma unroll

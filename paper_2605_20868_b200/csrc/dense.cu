@@ -21,6 +21,7 @@ struct DenseArgs {
   ckv_step st;
   int32_t group;     // units per rung-4 group
   int32_t n_dsplit;  // splits per unit
+  int32_t blk_per_split;
 };
 
 __device__ __forceinline__ float dninf() { return __int_as_float(0xff800000); }
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   const int nh = st.n_heads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = c.n_blocks[u];
-  const int b0 = sp * (DN_TOK / B), b1 = min(nb, b0 + DN_TOK / B);
+  const int b0 = sp * a.blk_per_split, b1 = min(nb, b0 + a.blk_per_split);
   float* outp = st.dense_part + (((size_t)item * a.n_dsplit + sp) * H) * 132;
   if (b0 >= b1) {
     for (int i = tid; i < H * 132; i += blockDim.x) outp[i] = (i % 132 == 0) ? dninf() : 0.f;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   }
 }
 
-__global__ void k_dense_merge(DenseArgs a) {
+__global__ void __launch_bounds__(128) k_dense_merge(DenseArgs a) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int item = blockIdx.x;
@@ -181,27 +182,45 @@ __global__ void k_dense_merge(DenseArgs a) {
   const int nh = st.n_heads;
   const int tid = threadIdx.x;
   const int pl = c.partial_len[u];
+  const int ns = a.n_dsplit;
+  __shared__ float sm_m[H][160], sm_sc[H][160];
+  __shared__ float red[H][4];
+  const float* p0 = st.dense_part + ((size_t)item * ns * H) * 132;
+  // per-split maxima -> per-head frame, splits spread over the threads
+  for (int i = tid; i < ns * H; i += blockDim.x) sm_m[i % H][i / H] = p0[(size_t)i * 132];
+  __syncthreads();
+  if (tid < H * 32) {
+    const int h = tid >> 5, l = tid & 31;
+    float m = dninf();
+    for (int s = l; s < ns; s += 32) m = fmaxf(m, sm_m[h][s]);
+    m = warp_max(m);
+    if (l == 0) red[h][0] = m;
+  }
+  __syncthreads();
+  for (int i = tid; i < ns * H; i += blockDim.x) {
+    const int h = i % H, s = i / H;
+    const HeadState& hs =
+        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + (h < nh ? h : 0)) * CKV_HEAD_FLOATS);
+    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
+    sm_sc[h][s] = (sm_m[h][s] == dninf()) ? 0.f : expf(sm_m[h][s] - M);
+  }
+  __syncthreads();
   for (int h = 0; h < nh; ++h) {
     if (!((mask >> h) & 1)) continue;
     const HeadState& hs =
         *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + h) * CKV_HEAD_FLOATS);
-    const float mp = hs.mp, lp = hs.lp;
-    const float* np_ = hs.np_;
-    const float* p0 = st.dense_part + ((size_t)item * a.n_dsplit * H) * 132;
-    float M = (pl > 0) ? mp : dninf();
-    for (int s = 0; s < a.n_dsplit; ++s) M = fmaxf(M, p0[(s * H + h) * 132]);
+    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
     float L = 0.f, O = 0.f;
-    for (int s = 0; s < a.n_dsplit; ++s) {
+    for (int s = 0; s < ns; ++s) {
       const float* p = p0 + (s * H + h) * 132;
-      if (p[0] == dninf()) continue;
-      const float sc = expf(p[0] - M);
+      const float sc = sm_sc[h][s];
       L += p[1] * sc;
       O += p[4 + tid] * sc;
     }
     if (pl > 0) {
-      const float sc = expf(mp - M);
-      L += lp * sc;
-      O += np_[tid] * sc;
+      const float sc = expf(hs.mp - M);
+      L += hs.lp * sc;
+      O += hs.np_[tid] * sc;
     }
     st.out[((size_t)u * nh + h) * D + tid] = O / L;
   }
@@ -210,8 +229,12 @@ __global__ void k_dense_merge(DenseArgs a) {
 extern int g_launches;
 
 cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_tokens, cudaStream_t s) {
-  DenseArgs a{*c, *st, st->rung4_group > 0 ? st->rung4_group : c->n_units, 0};
-  a.n_dsplit = (host_max_tokens + DN_TOK - 1) / DN_TOK;  // full blocks only; partial via head state
+  DenseArgs a{*c, *st, st->rung4_group > 0 ? st->rung4_group : c->n_units, 0, DN_TOK / B};
+  // full blocks only (the partial block comes from the head state); at most
+  // 160 splits so the merge fits its shared buffers
+  const int nblk = (host_max_tokens + B - 1) / B;
+  while ((nblk + a.blk_per_split - 1) / a.blk_per_split > 160) a.blk_per_split *= 2;
+  a.n_dsplit = (nblk + a.blk_per_split - 1) / a.blk_per_split;
   if (a.n_dsplit < 1) a.n_dsplit = 1;
   if (a.n_dsplit > st->n_dsplit_cap) a.n_dsplit = st->n_dsplit_cap;
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t), s);

@@ -99,7 +99,7 @@ struct PassBSmem {
   float al[PB_WARPS][H];
 };
 
-__global__ void __launch_bounds__(PB_WARPS * 32) k_pass_b(StepArgs a) {
+__global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
   const ckv_cache& c = a.c;
