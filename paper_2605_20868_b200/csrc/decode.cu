@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
 // =============================================================================
 // select
 // =============================================================================
-constexpr int SEL_THREADS = 512;
+constexpr int SEL_THREADS = 256;
 constexpr int SEL_MAXSORT = 1024;
 
 __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
@@ -319,14 +319,14 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   __syncthreads();
 
   // ---- partial block on originals (attention.py:98-104) ------------------------
-  if (warp < pl) {
-    const uint16_t* pk = c.partial_k + ((size_t)u * B + warp) * D;
+  for (int t = warp; t < pl; t += SEL_THREADS / 32) {
+    const uint16_t* pk = c.partial_k + ((size_t)u * B + t) * D;
     float acc = 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       acc = fmaf(__half2float(__ushort_as_half(pk[lane * 4 + j])), S.qv[lane * 4 + j], acc);
     acc = warp_sum(acc);
-    if (lane == 0) S.ps[warp] = acc;
+    if (lane == 0) S.ps[t] = acc;
   }
   __syncthreads();
   float mp = ninf(), lp = 0.f;
@@ -647,9 +647,9 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
-    cudaFuncSetAttribute(k_select<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
   const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
@@ -661,12 +661,12 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
-  if (nbh <= SEL_THREADS * 16)
-    k_select<16><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
-  else if (nbh <= SEL_THREADS * 32)
+  if (nbh <= SEL_THREADS * 32)
     k_select<32><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
-  else
+  else if (nbh <= SEL_THREADS * 64)
     k_select<64><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+  else
+    k_select<128><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
