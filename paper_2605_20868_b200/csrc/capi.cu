@@ -66,7 +66,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
       pol->ranking_depth < 1 || pol->ranking_depth > 64)
     return CKV_EINVAL;
   long long work = (long long)n_units * max_blocks / 1184;
-  int bps = 128;
+  int bps = 256;
   while (bps > 16 && bps > work) bps >>= 1;
   st->n_heads = n_heads;
   st->blocks_per_split = bps;
@@ -76,6 +76,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->items_per_chunk = 32;
   st->n_chunks = 4 * ((st->kcap + 31) / 32);
   if (st->n_chunks < 4) st->n_chunks = 4;
+  if (st->n_chunks > 256) st->n_chunks = 256;
   st->n_dsplit_cap = (max_blocks * CKV_BLOCK + CKV_BLOCK + 2047) / 2048;
   return CKV_OK;
 }

@@ -341,23 +341,31 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     hs.np_[tid] = acc;
   }
 
-  // ---- merge the pass-A splits ---------------------------------------------------
+  // ---- merge the pass-A splits: headers in parallel, then independent loads ---------
   const int nsp = (nb + st.blocks_per_split - 1) / st.blocks_per_split;
   {
-    float M = ninf(), dm = 0.f;
-    for (int s = 0; s < nsp; ++s) {
-      const float* sp = st.split_state + (((size_t)u * st.n_splits + s) * H + h) * CKV_SPLIT_FLOATS;
-      M = fmaxf(M, sp[0]);
-      dm = fmaxf(dm, sp[2]);
+    const float* spb = st.split_state + (((size_t)u * st.n_splits) * H + h) * CKV_SPLIT_FLOATS;
+    float mloc = ninf(), dloc = 0.f;
+    for (int s2 = tid; s2 < nsp; s2 += SEL_THREADS) {
+      const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
+      mloc = fmaxf(mloc, sp[0]);
+      dloc = fmaxf(dloc, sp[2]);
     }
+    const float M = block_max_f(mloc, S.redf);
+    const float dm = block_max_f(dloc, S.redf);
+    for (int s2 = tid; s2 < nsp; s2 += SEL_THREADS) {
+      const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
+      S.cum[s2] = (sp[0] == ninf()) ? 0.0 : (double)expf(sp[0] - M);
+    }
+    __syncthreads();
     float L = 0.f, O = 0.f;
-    if (M != ninf()) {
-      for (int s = 0; s < nsp; ++s) {
-        const float* sp = st.split_state + (((size_t)u * st.n_splits + s) * H + h) * CKV_SPLIT_FLOATS;
-        if (sp[0] == ninf()) continue;
-        const float sc = expf(sp[0] - M);
+    if (M != ninf() && tid < D) {
+#pragma unroll 8
+      for (int s2 = 0; s2 < nsp; ++s2) {
+        const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
+        const float sc = (float)S.cum[s2];
         L += sp[1] * sc;
-        if (tid < D) O += sp[4 + tid] * sc;
+        O += sp[4 + tid] * sc;
       }
     }
     if (tid < D) hs.oA[tid] = O;
@@ -368,6 +376,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       hs.mp = mp;
       hs.lp = lp;
     }
+    __syncthreads();
   }
 
   // ---- this thread's blocks [tid*KPT, tid*KPT+KPT): order keys of l'_b in registers

@@ -357,9 +357,22 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   auto chunk = [&](int k) -> const float* {
     return st.chunk_state + (((size_t)u * C + k) * H + h) * CKV_CHUNK_FLOATS;
   };
-  float M = (hs.lA > 0.f) ? hs.mA : ninf();
-  for (int k = 0; k < C; ++k) M = fmaxf(M, chunk(k)[0]);
+  __shared__ float cm[256], csc[256];
+  __shared__ float red[8];
+  // chunk frames: headers in parallel, one max, then independent loads per channel
+  float ml = ninf();
+  for (int k = tid; k < C; k += blockDim.x) {
+    cm[k] = chunk(k)[0];
+    ml = fmaxf(ml, cm[k]);
+  }
+  ml = warp_max(ml);
+  if ((tid & 31) == 0) red[tid >> 5] = ml;
+  __syncthreads();
+  float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  if (hs.lA > 0.f) M = fmaxf(M, hs.mA);
   if (pl > 0) M = fmaxf(M, hs.mp);
+  for (int k = tid; k < C; k += blockDim.x) csc[k] = (cm[k] == ninf()) ? 0.f : expf(cm[k] - M);
+  __syncthreads();
   float den = 0.f, num = 0.f;
   if (hs.lA > 0.f) {
     const float sc = expf(hs.mA - M);
@@ -368,15 +381,21 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   }
   float canary = 0.f;
   double eF = 0.0, sF = 0.0;
+#pragma unroll 4
   for (int k = 0; k < C; ++k) {
     const float* cs = chunk(k);
-    if (cs[0] == ninf()) continue;
-    const float sc = expf(cs[0] - M);
+    const float sc = csc[k];
     den += cs[1] * sc;
     num += cs[8 + tid] * sc;
-    canary = fmaxf(canary, cs[2]);
-    eF += reinterpret_cast<const double*>(cs + 4)[0];
-    sF += reinterpret_cast<const double*>(cs + 4)[1];
+  }
+  if (tid == 0) {
+    for (int k = 0; k < C; ++k) {
+      if (cm[k] == ninf()) continue;
+      const float* cs = chunk(k);
+      canary = fmaxf(canary, cs[2]);
+      eF += reinterpret_cast<const double*>(cs + 4)[0];
+      sF += reinterpret_cast<const double*>(cs + 4)[1];
+    }
   }
   if (pl > 0) {
     const float sc = expf(hs.mp - M);
