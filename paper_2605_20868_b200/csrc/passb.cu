@@ -92,6 +92,7 @@ constexpr int PB_IPC = 32;  // work items per chunk
 
 struct PassBSmem {
   uint8_t rec[PB_WARPS][2][REC];
+  uint8_t kt[PB_WARPS][2][B * D * 2];  // FP16 Tier-2 key tile (fragment order) of promoted blocks
   uint64_t bar[PB_WARPS][2];
   float qh[H * D];
   float wn[PB_WARPS][B][H];
@@ -161,20 +162,24 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
     return (idx < cend) ? idx : -1;
   };
   const uint8_t* t1base = c.tier1 + ubk * REC;
+  // stage = the Tier-1 record (+ the FP16 key tile when some head promotes the block)
+  auto issue = [&](int item, int stg) {
+    const int e2 = work[item];
+    const int b2 = e2 & 0xffffff;
+    const bool keys = ((uint32_t)e2 >> 24) & 0xfu;
+    mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
+    bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
+    if (keys)
+      bulk_g2s(S.kt[warp][stg], c.tier2_k + (ubk + b2) * B * D, B * D * 2, &S.bar[warp][stg]);
+  };
   int cur = item_at(0);
-  if (lane == 0 && cur >= 0) {
-    const int b = work[cur] & 0xffffff;
-    mbar_expect_tx(&S.bar[warp][0], REC);
-    bulk_g2s(S.rec[warp][0], t1base + (size_t)b * REC, REC, &S.bar[warp][0]);
-  }
+  if (lane == 0 && cur >= 0) issue(cur, 0);
   for (int k = 0; cur >= 0; ++k) {
     const int stg = k & 1;
     const int nxt = item_at(k + 1);
     if (lane == 0 && nxt >= 0) {
-      const int b2 = work[nxt] & 0xffffff;
       fence_proxy_async();
-      mbar_expect_tx(&S.bar[warp][stg ^ 1], REC);
-      bulk_g2s(S.rec[warp][stg ^ 1], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg ^ 1]);
+      issue(nxt, stg ^ 1);
     }
     const int e = work[cur];
     const int b = e & 0xffffff;
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
     const BlockScores r = phase1_block(f, rec, smax, lane);
     float sn0 = r.s0, sn1 = r.s1;
     if (fm) {
-      const float2 so = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
+      const float2 so = orig_block(f16, reinterpret_cast<const uint4*>(S.kt[warp][stg]), lane);
       if (inF) {
         sn0 = so.x;
         sn1 = so.y;

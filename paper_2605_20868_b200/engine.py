@@ -104,6 +104,8 @@ class CertifiedDecoder:
         if scratch is not None:
             scratch.bind(cache)
         self.cert_host = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
+        self.status_host = torch.zeros((8,), dtype=torch.int32).pin_memory()
+        self.ps_host = torch.zeros((U, 4), dtype=torch.int32).pin_memory()
 
     # -- the device step -----------------------------------------------------
     def launch(self, queries=None):
@@ -130,8 +132,11 @@ class CertifiedDecoder:
                 "exploration spot checks are not on the device path yet; use exploration_rate=0")
         self.launch(queries)
         self.cert_host.copy_(self.cert_buf, non_blocking=True)
-        torch.cuda.current_stream(self.cache.device).synchronize()
-        st = self.cache.status.cpu()
+        self.status_host.copy_(self.cache.status, non_blocking=True)
+        if self.scratch is not None:
+            self.ps_host.copy_(self.page_stats, non_blocking=True)
+        torch.cuda.current_stream(self.cache.device).synchronize()  # the step's only host sync
+        st = self.status_host
         if st[_lib.ST_TIER2]:
             self.cache.status[_lib.ST_TIER2] = 0
             raise Tier2UnavailableError("full-precision originals of a promoted block are unavailable")
@@ -142,7 +147,7 @@ class CertifiedDecoder:
         for g0 in range(0, U, g):
             if (kinds[g0:g0 + g] == 2).any():
                 staging += min(g, U - g0) * 2 * self.cache.num_tokens * D * 2
-        ps = self.page_stats.cpu().numpy().copy() if self.scratch is not None else None
+        ps = self.ps_host.numpy().copy() if self.scratch is not None else None
         return StepOutput(self.out, cert, kinds, ps, staging, self)
 
 
