@@ -122,6 +122,7 @@ typedef struct {
 #define CKV_F_CLAMPED (1u << 5)
 #define CKV_F_NUMERIC (1u << 6)   /* non-finite fast-path output -> rung 4 (precondition) */
 #define CKV_F_ACTIVE (1u << 7)
+#define CKV_F_EXPLORE (1u << 8)   /* rung 4, cause canary, from the exploration spot check */
 
 /* Caller-owned per-step buffers (device memory). */
 typedef struct {
@@ -151,6 +152,9 @@ typedef struct {
   int32_t n_dsplit_cap;     /* dense-fallback splits per unit (from ckv_plan) */
   int32_t* dense_list;      /* [1 + n_units] count, then unit | head_mask << 24 */
   float* dense_part;        /* [n_units][n_dsplit_cap][4][132] dense split states */
+  int32_t ecap;             /* exploration samples per head (capacity) */
+  int32_t* explore_n;       /* [n_units][n_heads] samples drawn by the host, or NULL */
+  int32_t* explore_pos;     /* [n_units][n_heads][ecap] ascending tail positions */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136
@@ -192,6 +196,17 @@ ckv_status ckv_reset(const ckv_cache* c, void* stream);
 ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                            const ckv_scratch* scratch, int32_t host_max_blocks,
                            void* stream);
+
+/* The step in two halves, for callers that must read the decisions before
+ * finishing it (the exploration spot check draws its host-side Philox samples
+ * from the tail size K' reported by the first half):
+ *   ckv_decode_begin: pass A, selection, pass B, combine (certificates written)
+ *   ckv_decode_end:   exploration (when st->explore_n), step-wide rung 4,
+ *                     dense fallback, LRU accounting (when scratch). */
+ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                            int32_t host_max_blocks, void* stream);
+ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
 
 /* Unpack Tier-1 for parity: codes i8 [nb][16][128], kscale/koffset f32 [nb][128],
  * vcodes u8 [nb][16][128], vscale/voffset fp16 [nb][16][8], for blocks

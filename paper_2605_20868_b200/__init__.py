@@ -13,6 +13,6 @@ from .cache import (DeviceKVCache, ScratchCache, StorageReport, TieredCache, sto
 from .engine import (CertifiedDecoder, HeadStepResult, StepOutput, dense_attention,
                      run_decode_step)
 from .errors import EmptyCacheError, PagingError, Tier2UnavailableError
-from .harness import (RunResult, Workload, WorkloadConfig, aggregate_telemetry,
-                      generate_workload, gqa_union, run_workload)
+from .harness import (RunResult, Workload, WorkloadConfig, aggregate_telemetry, dump_line,
+                      generate_workload, gqa_union, run_workload, write_telemetry)
 from .policy import Certificate, FallbackEvent, PolicyConfig, RungFlags

@@ -24,6 +24,7 @@ ST_NONFINITE, ST_CAPACITY, ST_TIER2 = 0, 1, 2
 
 F_RUNG1, F_RUNG2, F_RANKING, F_BOUNDARY = 1, 2, 4, 8
 F_CANARY, F_CLAMPED, F_NUMERIC, F_ACTIVE = 16, 32, 64, 128
+F_EXPLORE = 256
 
 STATUS = {0: "CKV_OK", 1: "CKV_EINVAL", 2: "CKV_EMPTY", 3: "CKV_ECAPACITY",
           4: "CKV_EPAGING", 5: "CKV_ETIER2", 6: "CKV_ENONFINITE", 7: "CKV_ECUDA"}
@@ -60,7 +61,8 @@ class CkvStep(ctypes.Structure):
                 ("out", P), ("cert", P), ("lm1", P), ("split_state", P), ("order", P),
                 ("work", P), ("n_work", P), ("vlist", P), ("lm2", P), ("head_state", P),
                 ("chunk_state", P), ("page_stats", P), ("prof_begin", P), ("prof_end", P),
-                ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P)]
+                ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P),
+                ("ecap", I32), ("explore_n", P), ("explore_pos", P)]
 
 
 class CkvScratch(ctypes.Structure):
@@ -92,6 +94,10 @@ def load():
         "ckv_reset": (I32, [ctypes.POINTER(CkvCache), P]),
         "ckv_decode_step": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
                                   ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
+        "ckv_decode_begin": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
+                                   ctypes.POINTER(CkvStep), I32, P]),
+        "ckv_decode_end": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
+                                 ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_read_tier1": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, P, P, P, P, P, P, P]),
         "ckv_fault_offset": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, ctypes.c_float, P]),
         "ckv_tier2_drop": (I32, [ctypes.POINTER(CkvCache), I32, I32, P]),
@@ -114,7 +120,7 @@ def exported_symbols():
     return ["ckv_version", "ckv_lru_words", "ckv_scratch_init", "ckv_plan", "ckv_append",
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
             "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
-            "ckv_f64_to_f16", "ckv_last_error"]
+            "ckv_f64_to_f16", "ckv_last_error", "ckv_decode_begin", "ckv_decode_end"]
 
 
 def check(code, what):

@@ -13,6 +13,7 @@ cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
 cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_dense(const ckv_cache*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
 int lru_ring(int, int);
@@ -93,16 +94,30 @@ ckv_status ckv_reset(const ckv_cache* c, void* stream) {
   return st_of(ckv::launch_reset(c, S(stream)));
 }
 
-ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                           const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+static bool step_ok(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                    int32_t host_max_blocks) {
   if (!cache_ok(c) || !pol || !st || !st->q || !st->out || !st->cert || !st->lm1 ||
       !st->split_state || !st->order || !st->work || !st->n_work || !st->vlist || !st->lm2 ||
       !st->head_state || !st->chunk_state || !st->dense_list || !st->dense_part)
-    return CKV_EINVAL;
-  if (host_max_blocks < 0 || host_max_blocks > c->max_blocks) return CKV_EINVAL;
-  if (pol->greedy_value_budget >= 0.0) return CKV_EINVAL;  // greedy rung 2 not on device yet
-  cudaError_t e = ckv::launch_decode(c, pol, st, host_max_blocks, S(stream));
-  if (e != cudaSuccess) return st_of(e);
+    return false;
+  return host_max_blocks >= 0 && host_max_blocks <= c->max_blocks;
+}
+
+ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                            int32_t host_max_blocks, void* stream) {
+  if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
+  return st_of(ckv::launch_decode(c, pol, st, host_max_blocks, S(stream)));
+}
+
+ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+  if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
+  cudaError_t e = cudaSuccess;
+  if (st->explore_n) {
+    if (!st->explore_pos || st->ecap <= 0) return CKV_EINVAL;
+    e = ckv::launch_explore(c, pol, st, host_max_blocks, S(stream));
+    if (e != cudaSuccess) return st_of(e);
+  }
   e = ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream));
   if (e != cudaSuccess) return st_of(e);
   if (scratch) {
@@ -112,6 +127,17 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
     if (e != cudaSuccess) return st_of(e);
   }
   return CKV_OK;
+}
+
+ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                           const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+  ckv_status r = ckv_decode_begin(c, pol, st, host_max_blocks, stream);
+  if (r != CKV_OK) return r;
+  const int32_t* en = st->explore_n;
+  st->explore_n = nullptr;  // samples need the begin half's K': use begin/end for exploration
+  r = ckv_decode_end(c, pol, st, scratch, host_max_blocks, stream);
+  st->explore_n = const_cast<int32_t*>(en);
+  return r;
 }
 
 ckv_status ckv_read_tier1(const ckv_cache* c, int32_t unit, int32_t b0, int32_t nb, int8_t* kcodes,

@@ -545,21 +545,77 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   // ---- tail mass, rung 2, E_val tail (fallback.py:141-161, certifier.py:153-160) ----
   const float* eta = c.eta + (size_t)u * c.max_blocks;
   const bool r2 = pol.rung2_enabled != 0;
+  const bool greedy = r2 && pol.greedy_value_budget >= 0.0;
+  // greedy budget mode: promote in descending p*eta (ties -> lower index) while the
+  // residual exceeds the budget; realised as a threshold T on the contribution key
+  // (all keys > T, plus the first `take` keys == T in block order)
+  uint32_t gT = 0xffffffffu;
+  int take = 0;
+  if (greedy && nb > 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j)
+      if (base + j < nb) tot += (double)(expf(ukey(kk[j]) - lsef) * eta[base + j]);
+    tot = block_sum_d(tot, S.redd);
+    const double need = tot - pol.greedy_value_budget;
+    if (need > 0.0) {
+      uint32_t lo = 0u;
+      unsigned long long hi = 0x100000000ull;
+      while (hi - lo > 1ull) {
+        const uint32_t mid = (uint32_t)((lo + hi) >> 1);
+        double g = 0.0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          if (base + j >= nb) continue;
+          const float cj = expf(ukey(kk[j]) - lsef) * eta[base + j];
+          if (__float_as_uint(cj) >= mid) g += (double)cj;
+        }
+        g = block_sum_d(g, S.redd);
+        if (g >= need) lo = mid;
+        else hi = mid;
+      }
+      gT = lo;
+      double ggt = 0.0;
+      int neq = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        if (base + j >= nb) continue;
+        const float cj = expf(ukey(kk[j]) - lsef) * eta[base + j];
+        if (__float_as_uint(cj) > gT) ggt += (double)cj;
+        neq += (__float_as_uint(cj) == gT);
+      }
+      ggt = block_sum_d(ggt, S.redd);
+      const int eq_before = block_excl_scan(neq, S.wsum, &S.misc[9]);
+      const double cT = (double)__uint_as_float(gT);
+      int m = (cT > 0.0) ? (int)ceil((need - ggt) / cT) : 0;
+      m = max(0, min(m, S.misc[9]));
+      take = m - eq_before;  // how many of this thread's == T blocks are promoted
+    }
+  }
   double at = 0.0, et = 0.0;
   int nv = 0;
-  uint32_t vbits = 0u;
+  uint32_t vb[(KPT + 31) / 32];
+#pragma unroll
+  for (int w = 0; w < (KPT + 31) / 32; ++w) vb[w] = 0u;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     const int b = base + j;
     if (b >= nb) continue;
-    const double pb = (double)expf(ukey(kk[j]) - lsef);
+    const float pf = expf(ukey(kk[j]) - lsef);
+    const double pb = (double)pf;
     const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
     const double pe = pb * (double)eta[b];
-    const bool inV = r2 && (pe > pol.v_tol);
+    bool inV;
+    if (greedy) {
+      const uint32_t ck = __float_as_uint(pf * eta[b]);
+      inV = (gT != 0xffffffffu) && (ck > gT || (ck == gT && take-- > 0));
+    } else {
+      inV = r2 && (pe > pol.v_tol);
+    }
     if (!inF) at += pb;
     if (!inF && !inV) et += pe;
     nv += inV;
-    vbits |= (uint32_t)inV << j;
+    vb[j >> 5] |= (uint32_t)inV << (j & 31);
   }
   at = block_sum_d(at, S.redd);
   et = block_sum_d(et, S.redd);
@@ -570,7 +626,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     int pv = vo;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
-      if ((vbits >> j) & 1u) vlist[pv++] = base + j;
+      if ((vb[j >> 5] >> (j & 31)) & 1u) vlist[pv++] = base + j;
   }
   if (tid == 0) {
     hs.lse = lse;
@@ -680,7 +736,6 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_passb(c, pol, st, s);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_block_logmass(const double* sc, const int64_t* bnd, int nb, double* bm,

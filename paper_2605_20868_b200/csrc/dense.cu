@@ -36,7 +36,7 @@ __global__ void k_resolve(DenseArgs a) {
   if (threadIdx.x == 0) any4 = 0;
   __syncthreads();
   for (int i = g0 * nh + threadIdx.x; i < g1 * nh; i += blockDim.x) {
-    if (st.cert[i].flags & (CKV_F_CANARY | CKV_F_NUMERIC)) any4 = 1;
+    if (st.cert[i].flags & (CKV_F_CANARY | CKV_F_NUMERIC | CKV_F_EXPLORE)) any4 = 1;
   }
   __syncthreads();
   for (int u = g0 + threadIdx.x; u < g1; u += blockDim.x) {

@@ -37,6 +37,7 @@ assert CERT_DTYPE.itemsize == ctypes.sizeof(_lib.CkvCert)
 class StepOutput:
     """Result of one batched certified decode step."""
     out: torch.Tensor            # [U, nh, 128] float32 (dense rungs applied)
+    explore_counts = None        # [U, nh] exploration samples (when the spot check ran)
     cert: np.ndarray             # [U, nh] CERT_DTYPE
     kinds: np.ndarray            # [U, nh] 0 quantized, 1 dense per head, 2 dense all heads
     page_stats: np.ndarray | None
@@ -88,6 +89,11 @@ class CertifiedDecoder:
                                        dtype=torch.float32, device=dev)
         self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
         self.dense_list = torch.zeros((U + 1,), dtype=torch.int32, device=dev)
+        st.ecap = max(1, int(round(0.05 * NB)) + 1)
+        self.explore_n = torch.zeros((U, nh), dtype=torch.int32, device=dev)
+        self.explore_pos = torch.zeros((U, nh, st.ecap), dtype=torch.int32, device=dev)
+        self.explore_n_host = torch.zeros((U, nh), dtype=torch.int32).pin_memory()
+        self.explore_pos_host = torch.zeros((U, nh, st.ecap), dtype=torch.int32).pin_memory()
         self.dense_part = torch.zeros((U, st.n_dsplit_cap, 4, 132), dtype=torch.float32, device=dev)
         for name, t in (("q", self.q), ("out", self.out), ("cert", self.cert_buf),
                         ("lm1", self.lm1), ("split_state", self.split_state),
@@ -95,7 +101,7 @@ class CertifiedDecoder:
                         ("vlist", self.vlist), ("lm2", self.lm2),
                         ("head_state", self.head_state), ("chunk_state", self.chunk_state),
                         ("page_stats", self.page_stats), ("dense_list", self.dense_list),
-                        ("dense_part", self.dense_part)):
+                        ("dense_part", self.dense_part), ("explore_pos", self.explore_pos)):
             setattr(st, name, _ptr(t))
         self.rung4_group = int(rung4_group or U)
         st.rung4_group = self.rung4_group
@@ -118,19 +124,26 @@ class CertifiedDecoder:
                                         _stream(self.cache.device))
         _lib.check(code, "ckv_decode_step")
 
-    def step(self, queries):
+    def step(self, queries, rng=None):
         """Certified attention for all units: queries [U, nh, 128] (float64).
 
         The fast path, the step-wide Rung 4 resolution and the dense fallback
-        all run on the device inside one ``ckv_decode_step``; the host reads
-        back the certificate array (and raises on a Tier-2 loss).
+        all run on the device; the host reads back the certificate array once
+        (and raises on a Tier-2 loss).  With ``policy.exploration_rate > 0``
+        and a NumPy Generator ``rng`` the exploration spot check runs between
+        the two halves of the step: the host draws the sampled tail positions
+        from ``rng`` exactly as fallback.py:212-218 does (heads in unit-major
+        q-head order) and the device rescores those blocks.
         """
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
-        if self.policy.exploration_rate > 0:
-            raise NotImplementedError(
-                "exploration spot checks are not on the device path yet; use exploration_rate=0")
+        self.explore_counts = None
+        if self.policy.exploration_rate > 0 and rng is not None:
+            return self._step_explore(queries, rng)
         self.launch(queries)
+        return self._finish()
+
+    def _finish(self):
         self.cert_host.copy_(self.cert_buf, non_blocking=True)
         self.status_host.copy_(self.cache.status, non_blocking=True)
         if self.scratch is not None:
@@ -149,6 +162,44 @@ class CertifiedDecoder:
                 staging += min(g, U - g0) * 2 * self.cache.num_tokens * D * 2
         ps = self.ps_host.numpy().copy() if self.scratch is not None else None
         return StepOutput(self.out, cert, kinds, ps, staging, self)
+
+    def _step_explore(self, queries, rng):
+        if queries is not None:
+            self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
+        stream = _stream(self.cache.device)
+        nbk = self.cache.num_blocks
+        _lib.check(self.lib.ckv_decode_begin(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
+                                             ctypes.byref(self.st), nbk, stream), "ckv_decode_begin")
+        self.cert_host.copy_(self.cert_buf, non_blocking=True)
+        torch.cuda.current_stream(self.cache.device).synchronize()
+        cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh)
+        en = self.explore_n_host.numpy()
+        ep = self.explore_pos_host.numpy()
+        en[:] = 0
+        rate = self.policy.exploration_rate
+        for u in range(self.cache.n_units):
+            for j in range(self.nh):
+                if not nbk:
+                    continue
+                n_tail = nbk - int(cert[u, j]["k_star"])
+                count = min(n_tail, int(round(rate * nbk)))
+                if count == 0:
+                    continue
+                chosen = np.sort(rng.choice(n_tail, size=count, replace=False))
+                en[u, j] = count
+                ep[u, j, :count] = chosen
+        self.explore_n.copy_(self.explore_n_host, non_blocking=True)
+        self.explore_pos.copy_(self.explore_pos_host, non_blocking=True)
+        self.st.explore_n = _ptr(self.explore_n)
+        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
+        code = self.lib.ckv_decode_end(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
+                                       ctypes.byref(self.st), sc, nbk, stream)
+        self.st.explore_n = None
+        _lib.check(code, "ckv_decode_end")
+        out = self._finish()
+        self.explore_counts = en.copy()
+        out.explore_counts = self.explore_counts
+        return out
 
 
 # -- reference-shaped per-head API --------------------------------------------
@@ -189,7 +240,7 @@ def certificate_from_row(row, head, step, kind=None):
         v_max=float(row["v_max"]), k_star=int(row["k_star"]), returned_kind=KINDS[kind],
         rung_flags=RungFlags(rung1=bool(fl & _lib.F_RUNG1), rung2=bool(fl & _lib.F_RUNG2),
                              rung3=bool(fl & (_lib.F_RANKING | _lib.F_BOUNDARY)),
-                             rung4=bool(fl & (_lib.F_CANARY | _lib.F_NUMERIC))))
+                             rung4=bool(fl & (_lib.F_CANARY | _lib.F_NUMERIC | _lib.F_EXPLORE))))
 
 
 def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, rng=None,
@@ -197,8 +248,6 @@ def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, 
     """One q-head through the certified pipeline (harness.py:186-300)."""
     if not isinstance(cache, TieredCache):
         raise TypeError("run_decode_step expects a paper_2605_20868_b200.TieredCache")
-    if policy.exploration_rate > 0 and rng is not None:
-        raise NotImplementedError("exploration spot checks are not on the device path yet")
     q = np.asarray(query, dtype=np.float64).reshape(-1)
     if q.shape[0] != cache.head_dim:
         raise ValueError(f"query has length {q.shape[0]}, expected {cache.head_dim}")
@@ -211,11 +260,10 @@ def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, 
     dkey = ("dec", policy, id(scratch))
     dec = cache.__dict__.get(dkey)
     if dec is None:
-        dec = CertifiedDecoder(cache.dev, dataclasses.replace(policy, exploration_rate=0.0),
-                               n_heads=1, scratch=scratch)
+        dec = CertifiedDecoder(cache.dev, policy, n_heads=1, scratch=scratch)
         cache.__dict__[dkey] = dec
     before = scratch.counters.sum(0).cpu().tolist() if scratch is not None else None
-    res = dec.step(torch.from_numpy(q).reshape(1, 1, D).to(cache.dev.device))
+    res = dec.step(torch.from_numpy(q).reshape(1, 1, D).to(cache.dev.device), rng=rng)
     row = res.cert[0, 0]
     kind = int(res.kinds[0, 0])
     cert = certificate_from_row(row, head, step, kind)
@@ -227,6 +275,9 @@ def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, 
             reports["keys"] = {"hits": d[0], "misses": d[1], "bytes": d[2]}
         if value_scratch is not None:
             reports["values"] = {"hits": d[3], "misses": d[4], "bytes": d[5]}
+    if res.explore_counts is not None:
+        n = int(res.explore_counts[0, 0])
+        reports["exploration"] = {"hits": 0, "misses": n, "bytes": n * B * D * 2}
     prom = res.promoted(0, 0)
     vprom = frozenset(int(b) for b in res.value_promotions(0, 0))
     decision = SelectionView(frozenset(int(b) for b in prom), int(row["k_star"]),
@@ -236,7 +287,8 @@ def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, 
     out = res.out[0, 0].double().cpu().numpy()
     return HeadStepResult(out, cert, events_from_flags(int(row["flags"]), head, step), reports,
                           decision, vprom, None, float(row["delta_h"]),
-                          rung4_requested=bool(int(row["flags"]) & (_lib.F_CANARY | _lib.F_NUMERIC)))
+                          rung4_requested=bool(int(row["flags"]) & (_lib.F_CANARY | _lib.F_NUMERIC
+                                                                    | _lib.F_EXPLORE)))
 
 
 def dense_attention(query, cache):

@@ -228,16 +228,15 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
     cfg = workload.config
     if cfg.group_factor > _lib.MAX_QHEADS:
         raise ValueError("device path supports up to 4 query heads per KV head")
-    if policy.exploration_rate > 0:
-        raise NotImplementedError("exploration spot checks are not on the device path yet")
     cache = workload.cache
+    explore_rng = _philox(cfg.seed, 1)  # harness.py:348
     scratch = ScratchCache(key_capacity, value_capacity)
     dec = CertifiedDecoder(cache, policy, n_heads=cfg.group_factor, scratch=scratch)
     gf = cfg.group_factor
     records, outputs = [], []
     for step in range(cfg.steps):
         q = torch.from_numpy(workload.queries[step].reshape(cfg.kv_heads, gf, cfg.head_dim))
-        res = dec.step(q.to(cache.device))
+        res = dec.step(q.to(cache.device), rng=explore_rng)
         certs, events = [], []
         for h in range(cfg.query_heads):
             u, j = divmod(h, gf)
@@ -253,6 +252,8 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
                     un.update(int(b) for b in res.promoted(u, j))
                 fr.append(len(un) / cache.num_blocks)
         bytes_paged = int(ps[1] + ps[3]) * _lib.BLOCK * _lib.HEAD_DIM * 2
+        if res.explore_counts is not None:
+            bytes_paged += int(res.explore_counts.sum()) * _lib.BLOCK * _lib.HEAD_DIM * 2
         records.append(step_record(step, certs, events, _scr(ps[0], ps[1]), _scr(ps[2], ps[3]),
                                    bytes_paged, res.staging_bytes, fr))
         if keep_outputs:
@@ -267,3 +268,40 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
     if keep_outputs:
         rr.outputs = outputs
     return rr
+
+
+def _jsonable(obj):
+    if isinstance(obj, dict):
+        return {k: _jsonable(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_jsonable(v) for v in obj]
+    if isinstance(obj, np.integer):
+        return int(obj)
+    if isinstance(obj, np.floating):
+        return float(obj)
+    if isinstance(obj, np.ndarray):
+        return [_jsonable(v) for v in obj.tolist()]
+    return obj
+
+
+def dump_line(obj):
+    """One deterministic JSONL line (cli.py:80-95: sorted keys, compact separators)."""
+    import json
+    return json.dumps(_jsonable(obj), sort_keys=True, separators=(",", ":"))
+
+
+def write_telemetry(result, path, config_path="", seed_override=None, version="0.1.0"):
+    """The bound report as the reference CLI writes it (cli.py:98-117): a header
+    line, one line per step record, one summary line."""
+    header = dict(result.header)
+    header["kind"] = "header"
+    header["manifest"] = {"config_path": config_path, "seed_override": seed_override}
+    header["rng"] = RNG_ALGORITHM
+    header["kernel_backend"] = "b200"
+    header["version"] = version
+    with open(path, "w") as fh:
+        fh.write(dump_line(header) + "\n")
+        for record in result.step_records:
+            fh.write(dump_line({"kind": "step", **record}) + "\n")
+        fh.write(dump_line({"kind": "summary", **result.summary}) + "\n")
+    return path

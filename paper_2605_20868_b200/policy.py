@@ -173,6 +173,8 @@ def events_from_flags(flags, head, step):
         ev.append(FallbackEvent(3, head, step, CAUSE_BOUNDARY))
     if flags & _lib.F_CANARY:
         ev.append(FallbackEvent(4, head, step, CAUSE_CANARY))
+    if flags & _lib.F_EXPLORE:
+        ev.append(FallbackEvent(4, head, step, CAUSE_CANARY))
     if flags & _lib.F_NUMERIC:
         ev.append(FallbackEvent(4, head, step, CAUSE_PRECONDITION))
     return ev

@@ -328,3 +328,34 @@ def test_host_tier2_matches_device_tier2(ck):
     for a, b in zip(outs[0][0], outs[1][0]):
         assert np.array_equal(a, b)
     assert outs[0][1] == outs[1][1]
+
+
+@pytest.mark.parametrize("name", ["explore", "greedy"])
+def test_exploration_and_greedy_parity(ck, name, tmp_path):
+    """Exploration spot checks (host Philox draws, device rescoring) and the greedy
+    Rung-2 budget mode against the oracle; the bound report is written as JSONL."""
+    if name == "explore":
+        wkw = dict(kind="gaussian", n_tokens=2400, query_heads=8, kv_heads=2, steps=3, seed=7)
+        pkw = dict(exploration_rate=0.05, k_max=8)
+    else:
+        wkw = dict(kind="sink", n_tokens=1500, query_heads=8, kv_heads=2, steps=2, seed=12)
+        pkw = dict(exploration_rate=0.0, greedy_value_budget=0.3)
+    cfg = ck.WorkloadConfig(head_dim=128, ingest_binary16=True, **wkw)
+    wl = ck.generate_workload(cfg)
+    dev = ck.run_workload(wl, ck.PolicyConfig(**pkw), 64, 64, keep_outputs=True)
+    ow = make_workload(head_dim=128, ingest_binary16=True, narrow=True, **wkw)
+    ref = oracle_run(ow, OraclePolicy(**pkw), 64, 64)
+    for s, (drec, orec) in enumerate(zip(dev.step_records, ref["records"])):
+        assert drec["events"] == orec["events"], (name, s)
+        assert drec["rung_counts"] == orec["rung_counts"]
+        assert drec["bytes_paged_in"] == orec["bytes_paged_in"]
+        assert drec["key_scratch"] == orec["key_scratch"]
+        assert drec["value_scratch"] == orec["value_scratch"]
+        for dc, oc in zip(drec["certificates"], orec["certificates"]):
+            assert dc["returned_kind"] == oc["returned_kind"]
+            assert _close(dc["e_val"], oc["e_val"]) and dc["k_star"] == oc["k_star"]
+    if name == "greedy":
+        assert sum(r["rung_counts"]["rung2"] for r in dev.step_records) > 0
+    path = ck.write_telemetry(dev, str(tmp_path / "run.jsonl"))
+    lines = open(path).read().splitlines()
+    assert len(lines) == cfg.steps + 2 and '"kernel_backend":"b200"' in lines[0]
