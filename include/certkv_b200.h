@@ -161,13 +161,23 @@ typedef struct {
 #define CKV_HEAD_FLOATS 288
 #define CKV_CHUNK_FLOATS 136
 
-/* Scratch (LRU page-in) state per unit; capacity in blocks for keys and values. */
+/* Scratch (LRU page-in) state per unit; capacity in blocks for keys and values.
+ * When key_slots / value_slots are given (Tier-2 in pinned host RAM), every
+ * miss is copied from Tier-2 into its HBM slot by a gather kernel on a side
+ * stream, joined by an event before pass B, which then reads promoted
+ * originals from the slots (ScratchCache.request, cache.py:261-286).  Without
+ * slots (Tier-2 already in HBM) only the reference accounting runs. */
 typedef struct {
   int32_t key_capacity;
   int32_t value_capacity;
   int32_t* key_lru;         /* [n_units][ckv_lru_words(max_blocks, key_capacity)] */
   int32_t* value_lru;
   int64_t* counters;        /* [n_units][6] hits, misses, bytes for keys then values */
+  uint16_t* key_slots;      /* [n_units][key_capacity][16*128] fp16, or NULL */
+  uint16_t* value_slots;    /* [n_units][value_capacity][16*128] fp16, or NULL */
+  int32_t* miss_list;       /* [n_units][2][miss_cap] block ids paged in this step */
+  int32_t* miss_n;          /* [n_units][2] */
+  int32_t miss_cap;
 } ckv_scratch;
 
 /* Library / device info. */
@@ -200,13 +210,14 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
 /* The step in two halves, for callers that must read the decisions before
  * finishing it (the exploration spot check draws its host-side Philox samples
  * from the tail size K' reported by the first half):
- *   ckv_decode_begin: pass A, selection, pass B, combine (certificates written)
+ *   ckv_decode_begin: pass A, selection, LRU scratch + page-in (when scratch),
+ *                     pass B, combine (certificates written)
  *   ckv_decode_end:   exploration (when st->explore_n), step-wide rung 4,
- *                     dense fallback, LRU accounting (when scratch). */
+ *                     dense fallback. */
 ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                            int32_t host_max_blocks, void* stream);
+                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
+                          int32_t host_max_blocks, void* stream);
 
 /* Unpack Tier-1 for parity: codes i8 [nb][16][128], kscale/koffset f32 [nb][128],
  * vcodes u8 [nb][16][128], vscale/voffset fp16 [nb][16][8], for blocks

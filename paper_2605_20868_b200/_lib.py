@@ -67,7 +67,8 @@ class CkvStep(ctypes.Structure):
 
 class CkvScratch(ctypes.Structure):
     _fields_ = [("key_capacity", I32), ("value_capacity", I32), ("key_lru", P),
-                ("value_lru", P), ("counters", P)]
+                ("value_lru", P), ("counters", P), ("key_slots", P), ("value_slots", P),
+                ("miss_list", P), ("miss_n", P), ("miss_cap", I32)]
 
 
 CERT_DTYPE_FIELDS = [(n, t) for n, t in CkvCert._fields_]
@@ -95,9 +96,9 @@ def load():
         "ckv_decode_step": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
                                   ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_decode_begin": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
-                                   ctypes.POINTER(CkvStep), I32, P]),
+                                   ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_decode_end": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
-                                 ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
+                                 ctypes.POINTER(CkvStep), I32, P]),
         "ckv_read_tier1": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, P, P, P, P, P, P, P]),
         "ckv_fault_offset": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, ctypes.c_float, P]),
         "ckv_tier2_drop": (I32, [ctypes.POINTER(CkvCache), I32, I32, P]),

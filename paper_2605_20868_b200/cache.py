@@ -242,7 +242,9 @@ class ScratchCache:
         self.value_capacity = int(capacity if value_capacity is None else value_capacity)
         self._bound = None
 
-    def bind(self, cache):
+    def bind(self, cache, n_heads=4, kcap=258):
+        """Allocate the device LRU state (and, with Tier-2 in host RAM, the HBM
+        slot pool + miss lists of the side-stream page-in) for ``cache``."""
         if self._bound is cache:
             return
         lib = cache.lib
@@ -253,9 +255,23 @@ class ScratchCache:
         self.key_lru = torch.empty((U, wk), dtype=torch.int32, device=dev)
         self.value_lru = torch.empty((U, wv), dtype=torch.int32, device=dev)
         self.counters = torch.zeros((U, 6), dtype=torch.int64, device=dev)
-        self.c = _lib.CkvScratch(key_capacity=self.capacity, value_capacity=self.value_capacity,
+        self.key_slots = self.value_slots = self.miss_list = self.miss_n = None
+        miss_cap = 0
+        if cache.tier2_location == "host":
+            if self.capacity > 0:
+                self.key_slots = torch.empty((U, min(self.capacity, NB), B * D), dtype=torch.float16,
+                                             device=dev)
+            if self.value_capacity > 0:
+                self.value_slots = torch.empty((U, min(self.value_capacity, NB), B * D),
+                                               dtype=torch.float16, device=dev)
+            miss_cap = n_heads * (kcap + NB)
+            self.miss_list = torch.empty((U, 2, miss_cap), dtype=torch.int32, device=dev)
+            self.miss_n = torch.zeros((U, 2), dtype=torch.int32, device=dev)
+        self.c = _lib.CkvScratch(key_capacity=min(self.capacity, NB), value_capacity=min(self.value_capacity, NB),
                                  key_lru=_ptr(self.key_lru), value_lru=_ptr(self.value_lru),
-                                 counters=_ptr(self.counters))
+                                 counters=_ptr(self.counters), key_slots=_ptr(self.key_slots),
+                                 value_slots=_ptr(self.value_slots), miss_list=_ptr(self.miss_list),
+                                 miss_n=_ptr(self.miss_n), miss_cap=miss_cap)
         _lib.check(lib.ckv_scratch_init(U, NB, ctypes.byref(self.c), _stream(dev)),
                    "ckv_scratch_init")
         self._bound = cache

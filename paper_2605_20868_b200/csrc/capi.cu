@@ -11,12 +11,12 @@ cudaError_t launch_fault_offset(const ckv_cache*, int, int, int, float, cudaStre
 cudaError_t launch_tier2_drop(const ckv_cache*, int, int, cudaStream_t);
 cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
-cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, const ckv_scratch*, int,
+                          cudaStream_t);
 cudaError_t launch_dense(const ckv_cache*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
-int lru_ring(int, int);
 cudaError_t launch_block_logmass(const double*, const int64_t*, int, double*, double*, double*,
                                  cudaStream_t);
 cudaError_t launch_fused_attend(const float*, const float*, const int64_t*, int, int, float*, float*,
@@ -42,7 +42,7 @@ extern "C" {
 int32_t ckv_version(void) { return 100; }
 
 int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity) {
-  return 4 + max_blocks + ckv::lru_ring(max_blocks, capacity);
+  return ckv::lru_words(max_blocks, capacity);
 }
 
 ckv_status ckv_scratch_init(int32_t n_units, int32_t max_blocks, const ckv_scratch* sc,
@@ -104,13 +104,15 @@ static bool step_ok(const ckv_cache* c, const ckv_policy* pol, const ckv_step* s
 }
 
 ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                            int32_t host_max_blocks, void* stream) {
+                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
-  return st_of(ckv::launch_decode(c, pol, st, host_max_blocks, S(stream)));
+  if (scratch && (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters))
+    return CKV_EINVAL;
+  return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, S(stream)));
 }
 
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+                          int32_t host_max_blocks, void* stream) {
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   cudaError_t e = cudaSuccess;
   if (st->explore_n) {
@@ -119,24 +121,17 @@ ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* s
     if (e != cudaSuccess) return st_of(e);
   }
   e = ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream));
-  if (e != cudaSuccess) return st_of(e);
-  if (scratch) {
-    if (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters)
-      return CKV_EINVAL;
-    e = ckv::launch_scratch(c, st, scratch, S(stream));
-    if (e != cudaSuccess) return st_of(e);
-  }
-  return CKV_OK;
+  return st_of(e);
 }
 
 ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
-  ckv_status r = ckv_decode_begin(c, pol, st, host_max_blocks, stream);
+  ckv_status r = ckv_decode_begin(c, pol, st, scratch, host_max_blocks, stream);
   if (r != CKV_OK) return r;
-  const int32_t* en = st->explore_n;
+  int32_t* en = st->explore_n;
   st->explore_n = nullptr;  // samples need the begin half's K': use begin/end for exploration
-  r = ckv_decode_end(c, pol, st, scratch, host_max_blocks, stream);
-  st->explore_n = const_cast<int32_t*>(en);
+  r = ckv_decode_end(c, pol, st, host_max_blocks, stream);
+  st->explore_n = en;
   return r;
 }
 

@@ -56,6 +56,22 @@ __host__ __device__ inline int k2_offset(int t, int c) {
   return kt * 256 + lane * 8 + reg * 2 + (cc & 1);
 }
 
+// LRU ring size for a scratch of `cap` blocks (0 = no eviction possible); see scratch.cu
+__host__ __device__ inline int lru_ring(int max_blocks, int cap) {
+  if (cap >= max_blocks) return 0;
+  int need = 2 * cap + max_blocks + 1024;
+  int R = 1;
+  while (R < need) R <<= 1;
+  return R;
+}
+__host__ __device__ inline int lru_words(int max_blocks, int cap) {
+  return 4 + 2 * max_blocks + lru_ring(max_blocks, cap);
+}
+// slot table (HBM slot of each resident block, -1 otherwise) inside an LRU state
+__host__ __device__ inline int lru_slot_offset(int max_blocks, int cap) {
+  return 4 + max_blocks + lru_ring(max_blocks, cap);
+}
+
 // ---- bit helpers ------------------------------------------------------------
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }

@@ -702,12 +702,14 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // launchers
 // =============================================================================
 extern int g_launches;
-cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, cudaStream_t);
+cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&,
+                         cudaStream_t);
+cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                          int host_max_blocks, cudaStream_t s) {
+                          const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
   g_launches = 0;
-  StepArgs a{*c, *st, *pol};
+  StepArgs a{*c, *st, *pol, PageView{}};
   const size_t smA = sizeof(PassASmem);
   static bool attrs = false;
   if (!attrs) {
@@ -735,7 +737,20 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_passb(c, pol, st, s);
+  PageView pv{};
+  if (sc) {
+    e = launch_scratch(c, st, sc, s);  // LRU accounting (+ side-stream page-in into slots)
+    if (e != cudaSuccess) return e;
+    pv.kslots = sc->key_slots;
+    pv.vslots = sc->value_slots;
+    pv.kcap = sc->key_capacity;
+    pv.vcap = sc->value_capacity;
+    pv.kstride = lru_words(c->max_blocks, sc->key_capacity);
+    pv.vstride = lru_words(c->max_blocks, sc->value_capacity);
+    pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
+    pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
+  }
+  return launch_passb(c, pol, st, pv, s);
 }
 
 cudaError_t launch_block_logmass(const double* sc, const int64_t* bnd, int nb, double* bm,

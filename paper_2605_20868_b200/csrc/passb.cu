@@ -163,14 +163,20 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
   };
   const uint8_t* t1base = c.tier1 + ubk * REC;
   // stage = the Tier-1 record (+ the FP16 key tile when some head promotes the block)
+  const PageView& pv = a.pv;
+  const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
+  const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
+  auto key_src = [&](int b2) -> const uint16_t* {  // scratch slot if resident, else Tier-2
+    const int sl = kslot ? kslot[b2] : -1;
+    return (sl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + sl) * B * D : c.tier2_k + (ubk + b2) * B * D;
+  };
   auto issue = [&](int item, int stg) {
     const int e2 = work[item];
     const int b2 = e2 & 0xffffff;
     const bool keys = ((uint32_t)e2 >> 24) & 0xfu;
     mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
     bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
-    if (keys)
-      bulk_g2s(S.kt[warp][stg], c.tier2_k + (ubk + b2) * B * D, B * D * 2, &S.bar[warp][stg]);
+    if (keys) bulk_g2s(S.kt[warp][stg], key_src(b2), B * D * 2, &S.bar[warp][stg]);
   };
   int cur = item_at(0);
   if (lane == 0 && cur >= 0) issue(cur, 0);
@@ -253,7 +259,9 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
     const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
     const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
     const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(rec + OFF_VMETA + g * 64);
-    const uint16_t* vorig = c.tier2_v + (ubk + b) * B * D + lane * 4;
+    const int vsl = (vm && vslot) ? vslot[b] : -1;
+    const uint16_t* vorig = ((vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D
+                                        : c.tier2_v + (ubk + b) * B * D) + lane * 4;
 #pragma unroll 4
     for (int t = 0; t < B; ++t) {
       const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
@@ -478,8 +486,9 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
 
 extern int g_launches;
 
-cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st, cudaStream_t s) {
-  StepArgs a{*c, *st, *pol};
+cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                         const PageView& pv, cudaStream_t s) {
+  StepArgs a{*c, *st, *pol, pv};
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));

@@ -1,4 +1,4 @@
-// LRU scratch accounting for promoted originals, exact to ScratchCache.request
+// LRU scratch for promoted originals, exact to ScratchCache.request
 // (cache.py:243-312): per unit and per payload kind, the q-heads' requests are
 // processed in head order, each request list ascending; a hit moves the block
 // to MRU, a miss admits it at MRU and evicts the LRU entry past capacity; a
@@ -6,13 +6,19 @@
 //
 // State per (unit, kind), int32 words:  [0] T clock, [1] P oldest stamp,
 // [2] count, [3] R ring size (0 = capacity covers every block, no eviction
-// possible), [4 .. 4+max_blocks) stamp[b] (0 = absent), then ring[R] holding
-// the block id last stamped with s at ring[s & (R-1)].  Recency order is stamp
-// order; a ring slot is live iff stamp[ring[s]] == s, so a hit simply leaves a
-// stale slot behind.  Batches that cannot evict run fully parallel; batches
-// that must evict walk the ring from P sequentially (one thread, shared
-// memory), which is only reached when the scratch is smaller than the working
-// set -- the regime where the Tier-2 transfer dominates anyway.
+// possible), then stamp[max_blocks] (0 = absent), ring[R] (block id last
+// stamped with s at ring[s & (R-1)]), slot[max_blocks] (HBM slot of a resident
+// block, -1 otherwise).  Recency order is stamp order; a ring slot is live iff
+// stamp[ring[s]] == s, so a hit simply leaves a stale entry behind.  Batches
+// that cannot evict run fully parallel (misses take slots count, count+1, ...);
+// batches that must evict walk the ring from P sequentially (one thread,
+// shared memory) and hand the victim's slot to the new block -- only reached
+// when the scratch is smaller than the working set, the regime where the
+// Tier-2 transfer dominates anyway.
+//
+// k_pagein then copies every block missed this step that is still resident
+// from Tier-2 (pinned host RAM, read zero-copy over PCIe) into its slot; it
+// runs on a side stream joined by an event before pass B.
 #include "common.cuh"
 
 namespace ckv {
@@ -53,6 +59,9 @@ struct LruArgs {
   int32_t cap;
   int32_t kind;  // 0 keys, 1 values
   int64_t* counters;
+  int32_t* miss_list;  // [U][2][miss_cap]
+  int32_t* miss_n;     // [U][2]
+  int32_t miss_cap;
 };
 
 __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
@@ -66,21 +75,29 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   __shared__ int hdr[4];
   __shared__ int ws[32];
   __shared__ int misc[8];
+  __shared__ int nmiss;
   if (tid < 4) hdr[tid] = L[tid];
+  if (tid == 0) nmiss = 0;
   __syncthreads();
   const int R = hdr[3];
   const int M = R - 1;
   int32_t* stamp = sm;               // [maxb]
   int32_t* ring = sm + maxb;         // [R]
-  int32_t* req = ring + R;           // [maxb + 1024] request list
+  int32_t* slot = ring + R;          // [maxb]
+  int32_t* req = slot + maxb;        // [maxb + 1024] request list
   int32_t* tmp = req + maxb + 1024;  // [maxb] compaction buffer
   uint32_t* bits = reinterpret_cast<uint32_t*>(tmp + maxb);  // [maxb/32]
-  for (int i = tid; i < maxb; i += LRU_THREADS) stamp[i] = (i < nb) ? L[4 + i] : 0;
+  const int32_t* Lslot = L + 4 + maxb + R;
+  for (int i = tid; i < maxb; i += LRU_THREADS) {
+    stamp[i] = (i < nb) ? L[4 + i] : 0;
+    slot[i] = (i < nb) ? Lslot[i] : -1;
+  }
   for (int i = tid; i < R; i += LRU_THREADS) ring[i] = L[4 + maxb + i];
   __syncthreads();
   int T = hdr[0], P = hdr[1], count = hdr[2];
   const int cap = a.cap;
   long long hits = 0, misses = 0;
+  int32_t* mlist = a.miss_list ? a.miss_list + ((size_t)u * 2 + a.kind) * a.miss_cap : nullptr;
 
   for (int h = 0; h < st.n_heads; ++h) {
     const size_t hu = (size_t)u * st.n_heads + h;
@@ -135,24 +152,35 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
       P = 1;
       T = 1 + live;
     }
-    // ---- count misses -----------------------------------------------------------
+    // ---- count misses (contiguous chunks so ranks follow request order) -------
+    const int per = (n + LRU_THREADS - 1) / LRU_THREADS;
+    const int lo = tid * per, hi = min(n, lo + per);
     int m = 0;
-    for (int i = tid; i < n; i += LRU_THREADS) m += (stamp[req[i]] == 0);
-    int dummy = blk_scan_excl(m, ws, &misc[2]);
-    (void)dummy;
+    for (int i = lo; i < hi; ++i) m += (stamp[req[i]] == 0);
+    const int mrank = blk_scan_excl(m, ws, &misc[2]);
     const int nm = misc[2];
     if (cap > 0 && (R == 0 || count + nm <= cap)) {
-      for (int i = tid; i < n; i += LRU_THREADS) {
+      int r = mrank;
+      for (int i = lo; i < hi; ++i) {
         const int b = req[i];
+        if (stamp[b] == 0) {
+          slot[b] = count + r;
+          if (mlist) {
+            const int k = atomicAdd(&nmiss, 1);
+            if (k < a.miss_cap) mlist[k] = b;
+          }
+          ++r;
+        }
         stamp[b] = T + i;
         if (R > 0) ring[(T + i) & M] = b;
       }
+      __syncthreads();
       T += n;
       count += nm;
       hits += n - nm;
       misses += nm;
     } else if (cap == 0) {
-      misses += n;  // served, nothing retained
+      misses += n;  // served straight from Tier-2, nothing retained
     } else {
       if (tid == 0) {
         long long hh = 0, mm = 0;
@@ -162,19 +190,24 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
             ++hh;
           } else {
             ++mm;
+            int s;
             if (count == cap) {
               for (;;) {
                 const int v = ring[P & M];
                 if (v >= 0 && stamp[v] == P) {
                   stamp[v] = 0;
+                  s = slot[v];
+                  slot[v] = -1;
                   ++P;
                   break;
                 }
                 ++P;
               }
-              --count;
+            } else {
+              s = count++;
             }
-            ++count;
+            slot[b] = s;
+            if (mlist && nmiss < a.miss_cap) mlist[nmiss++] = b;
           }
           stamp[b] = T;
           ring[T & M] = b;
@@ -196,7 +229,11 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
     __syncthreads();
   }
   // ---- write back ---------------------------------------------------------------
-  for (int i = tid; i < nb; i += LRU_THREADS) L[4 + i] = stamp[i];
+  int32_t* Ls = L + 4 + maxb + R;
+  for (int i = tid; i < nb; i += LRU_THREADS) {
+    L[4 + i] = stamp[i];
+    Ls[i] = slot[i];
+  }
   for (int i = tid; i < R; i += LRU_THREADS) L[4 + maxb + i] = ring[i];
   if (tid == 0) {
     L[0] = T;
@@ -208,10 +245,34 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
     ctr[0] += hits;
     ctr[1] += misses;
     ctr[2] += misses * (long long)(B * D * 2);
+    if (a.miss_n) a.miss_n[u * 2 + a.kind] = min(nmiss, a.miss_cap);
   }
 }
 
-__global__ void k_lru_init(int32_t* state, int words, int maxb, int R, int n_units) {
+// gather: Tier-2 (pinned host, zero-copy) -> HBM slots for this step's misses
+__global__ void __launch_bounds__(256) k_pagein(ckv_cache c, ckv_scratch sc, int32_t kw, int32_t vw) {
+  const int u = blockIdx.x, kind = blockIdx.y, tid = threadIdx.x;
+  const int maxb = c.max_blocks;
+  const int cap = kind ? sc.value_capacity : sc.key_capacity;
+  uint16_t* slots = kind ? sc.value_slots : sc.key_slots;
+  if (!slots || cap <= 0) return;
+  const int words = kind ? vw : kw;
+  const int32_t* slot_of = (kind ? sc.value_lru : sc.key_lru) + (size_t)u * words + lru_slot_offset(maxb, cap);
+  const int n = sc.miss_n[u * 2 + kind];
+  const int32_t* ml = sc.miss_list + ((size_t)u * 2 + kind) * sc.miss_cap;
+  const uint16_t* src0 = kind ? c.tier2_v : c.tier2_k;
+  for (int k = 0; k < n; ++k) {
+    const int b = ml[k];
+    const int s = slot_of[b];
+    if (s < 0) continue;  // evicted again later in the same step: pass B reads Tier-2
+    if (tid == 0 && !c.tier2_valid[(size_t)u * maxb + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
+    const uint4* src = reinterpret_cast<const uint4*>(src0 + ((size_t)u * maxb + b) * B * D);
+    uint4* dst = reinterpret_cast<uint4*>(slots + ((size_t)u * cap + s) * B * D);
+    dst[tid] = src[tid];  // 256 threads x 16 B = one 4 KB block
+  }
+}
+
+__global__ void k_lru_init(int32_t* state, int words, int maxb, int R) {
   const int u = blockIdx.x;
   int32_t* L = state + (size_t)u * words;
   for (int i = threadIdx.x; i < words; i += blockDim.x) {
@@ -220,41 +281,58 @@ __global__ void k_lru_init(int32_t* state, int words, int maxb, int R, int n_uni
     else if (i == 2) v = 0;
     else if (i == 3) v = R;
     else if (i < 4 + maxb) v = 0;
-    else v = -1;
+    else v = -1;  // ring entries and slots
     L[i] = v;
   }
-  (void)n_units;
 }
 
-int lru_ring(int max_blocks, int cap) {
-  if (cap >= max_blocks) return 0;
-  int need = 2 * cap + max_blocks + 1024;
-  int R = 1;
-  while (R < need) R <<= 1;
-  return R;
+extern int g_launches;
+
+static cudaStream_t side_stream() {
+  static cudaStream_t s = nullptr;
+  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  return s;
 }
 
 cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc,
                            cudaStream_t s) {
-  extern int g_launches;
+  int words[2];
   for (int kind = 0; kind < 2; ++kind) {
     const int cap = kind ? sc->value_capacity : sc->key_capacity;
     const int R = lru_ring(c->max_blocks, cap);
-    const int words = 4 + c->max_blocks + R;
-    LruArgs a{*c, *st, kind ? sc->value_lru : sc->key_lru, words, cap, kind, sc->counters};
-    const size_t smem =
-        (size_t)(c->max_blocks + R + c->max_blocks + 1024 + c->max_blocks + (c->max_blocks + 31) / 32 + 4) * 4;
+    words[kind] = 4 + 2 * c->max_blocks + R;
+    LruArgs a{*c, *st, kind ? sc->value_lru : sc->key_lru, words[kind], cap, kind, sc->counters,
+              sc->miss_list, sc->miss_n, sc->miss_cap};
+    const size_t smem = (size_t)(c->max_blocks + R + c->max_blocks + c->max_blocks + 1024 +
+                                 c->max_blocks + (c->max_blocks + 31) / 32 + 4) * 4;
     cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_lru<<<c->n_units, LRU_THREADS, smem, s>>>(a);
     ++g_launches;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if ((sc->key_slots || sc->value_slots) && sc->miss_list && sc->miss_n) {
+    // page-in on a side stream: forked after the LRU, joined before pass B
+    cudaStream_t side = side_stream();
+    cudaEvent_t fork, join;
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    cudaEventRecord(fork, s);
+    cudaStreamWaitEvent(side, fork, 0);
+    k_pagein<<<dim3(c->n_units, 2), 256, 0, side>>>(*c, *sc, words[0], words[1]);
+    ++g_launches;
+    cudaEventRecord(join, side);
+    cudaStreamWaitEvent(s, join, 0);
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_lru_init(int32_t* state, int n_units, int max_blocks, int cap, cudaStream_t s) {
   const int R = lru_ring(max_blocks, cap);
-  const int words = 4 + max_blocks + R;
-  k_lru_init<<<n_units, 256, 0, s>>>(state, words, max_blocks, R, n_units);
+  const int words = 4 + 2 * max_blocks + R;
+  k_lru_init<<<n_units, 256, 0, s>>>(state, words, max_blocks, R);
   return cudaGetLastError();
 }
 

@@ -25,10 +25,21 @@ struct HeadState {
 static_assert(sizeof(HeadState) <= CKV_HEAD_FLOATS * 4, "head state too large");
 
 
+// Where pass B reads promoted originals from: HBM scratch slots (Tier-2 in host
+// RAM, blocks resident after this step's LRU) or Tier-2 itself.
+struct PageView {
+  const uint16_t* kslots;
+  const uint16_t* vslots;
+  const int32_t* kslot_of;  // per unit: + u * kstride
+  const int32_t* vslot_of;
+  int32_t kstride, vstride, kcap, vcap;
+};
+
 struct StepArgs {
   ckv_cache c;
   ckv_step st;
   ckv_policy pol;
+  PageView pv;
 };
 
 __device__ __forceinline__ float ninf() { return __int_as_float(0xff800000); }

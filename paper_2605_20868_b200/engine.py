@@ -108,7 +108,7 @@ class CertifiedDecoder:
         self.st = st
         self.scratch = scratch
         if scratch is not None:
-            scratch.bind(cache)
+            scratch.bind(cache, n_heads=self.nh, kcap=st.kcap)
         self.cert_host = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
         self.status_host = torch.zeros((8,), dtype=torch.int32).pin_memory()
         self.ps_host = torch.zeros((U, 4), dtype=torch.int32).pin_memory()
@@ -168,8 +168,9 @@ class CertifiedDecoder:
             self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
         stream = _stream(self.cache.device)
         nbk = self.cache.num_blocks
+        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
         _lib.check(self.lib.ckv_decode_begin(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                             ctypes.byref(self.st), nbk, stream), "ckv_decode_begin")
+                                             ctypes.byref(self.st), sc, nbk, stream), "ckv_decode_begin")
         self.cert_host.copy_(self.cert_buf, non_blocking=True)
         torch.cuda.current_stream(self.cache.device).synchronize()
         cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh)
@@ -191,9 +192,8 @@ class CertifiedDecoder:
         self.explore_n.copy_(self.explore_n_host, non_blocking=True)
         self.explore_pos.copy_(self.explore_pos_host, non_blocking=True)
         self.st.explore_n = _ptr(self.explore_n)
-        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
         code = self.lib.ckv_decode_end(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                       ctypes.byref(self.st), sc, nbk, stream)
+                                       ctypes.byref(self.st), nbk, stream)
         self.st.explore_n = None
         _lib.check(code, "ckv_decode_end")
         out = self._finish()
