@@ -37,6 +37,20 @@ def _k2_index():
 K2_INDEX = _k2_index()
 
 
+def _v2_index():
+    """natural [t][c] -> position in the fragment-ordered Tier-2 value block
+    (v2_offset in csrc/common.cuh)."""
+    t = np.arange(B)[:, None]
+    c = np.arange(D)[None, :]
+    g, r = c >> 4, c & 15
+    lane = (r & 7) * 4 + ((t & 7) >> 1)
+    reg = (r >> 3) + 2 * (t >> 3)
+    return (g * 256 + lane * 8 + reg * 2 + (t & 1)).reshape(-1)
+
+
+V2_INDEX = _v2_index()
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -216,6 +230,7 @@ class DeviceKVCache:
             v = v.to(self.device, non_blocking=True)
         idx = torch.as_tensor(K2_INDEX, device=k.device)
         k = k.reshape(-1, B * D)[:, idx].reshape(-1, D)  # fragment order -> [token][channel]
+        v = v.reshape(-1, B * D)[:, torch.as_tensor(V2_INDEX, device=v.device)].reshape(-1, D)
         p = self.partial_len
         if p:
             k = torch.cat([k, self.partial_k[unit, :p]], 0)

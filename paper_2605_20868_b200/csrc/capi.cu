@@ -74,9 +74,9 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->n_splits = (max_blocks + bps - 1) / bps;
   st->kcap = 2 * pol->k_max + 2;
   st->wcap = st->kcap + max_blocks;
-  st->items_per_chunk = 32;
-  st->n_chunks = 4 * ((st->kcap + 31) / 32);
-  if (st->n_chunks < 4) st->n_chunks = 4;
+  st->items_per_chunk = 128;
+  st->n_chunks = (4 * st->kcap + 127) / 128;
+  if (st->n_chunks < 1) st->n_chunks = 1;
   if (st->n_chunks > 256) st->n_chunks = 256;
   st->n_dsplit_cap = (max_blocks * CKV_BLOCK + CKV_BLOCK + 2047) / 2048;
   return CKV_OK;

@@ -22,14 +22,23 @@ constexpr int REC = CKV_BLOCK_BYTES;
 //                 row l/4 cols 16+4(l%4)+0..3, row l/4+8 same cols}
 //   [2048, 2560) key scale  f32[128]
 //   [2560, 3072) key offset f32[128]
-//   [3072, 4096) value codes: [half h][lane l][token 8h+i] u16 holding the
-//                nibbles of channels 4l..4l+3 (channel 4l+j at bits 4j)
-//   [4096, 4608) value meta: [group g][token t] half2(scale, offset)
+//   [3072, 4096) value codes, mma.m16n8k16 A-fragment order of V^T per value
+//                group g (rows = the group's 16 channels, k = the 16 tokens):
+//                word [g/4][lane l][g%4] (u32) holds the 8 nibbles lane l
+//                feeds for group g: channel 16g + l/4 (+8 for bits 8-15 /
+//                24-31), tokens 2(l%4) (+1 in the upper half-word, +8 for
+//                bits 4-7 / 20-23).  (w & 0x000f000f) is then a half2 of two
+//                codes, (w & 0x00f000f0) one of codes x 16, shifted by 8 the
+//                same for the upper channel.
+//   [4096, 4352) value scale  fp16 [j][g][i]  (j = (t%8)/2, i = t%2 + 2(t/8))
+//   [4352, 4608) value offset fp16 [j][g][i]  so lane l reads the (t, t+1),
+//                (t+8, t+9) pairs of its k-columns with one 8-byte load
 constexpr int OFF_KCODES = 0;
 constexpr int OFF_KSCALE = 2048;
 constexpr int OFF_KOFF = 2560;
 constexpr int OFF_VCODES = 3072;
-constexpr int OFF_VMETA = 4096;
+constexpr int OFF_VSCALE = 4096;
+constexpr int OFF_VOFF = 4352;
 
 __host__ __device__ inline int kcode_offset(int t, int c) {
   int kt = c >> 5, cc = c & 31;
@@ -37,23 +46,39 @@ __host__ __device__ inline int kcode_offset(int t, int c) {
   int reg = (t >> 3) + 2 * (cc >> 4);
   return OFF_KCODES + kt * 512 + lane * 16 + reg * 4 + (cc & 3);
 }
-__host__ __device__ inline int vcode_offset(int t, int c) {  // byte holding channel c's nibble pair
-  int l = c >> 2;
-  return OFF_VCODES + (t >> 3) * 512 + l * 16 + (t & 7) * 2 + ((c & 3) >> 1);
+// byte offset of the u32 word holding the nibble of value code (t, c), and its bit
+__host__ __device__ inline int vcode_word(int t, int c) {
+  int g = c >> 4, r = c & 15;
+  int lane = (r & 7) * 4 + ((t & 7) >> 1);
+  return OFF_VCODES + (g >> 2) * 512 + lane * 16 + (g & 3) * 4;
 }
-__host__ __device__ inline int vmeta_offset(int t, int g) { return OFF_VMETA + (g * 16 + t) * 4; }
+__host__ __device__ inline int vcode_bit(int t, int c) {
+  return 16 * (t & 1) + 4 * (t >> 3) + 8 * ((c & 15) >> 3);
+}
+__host__ __device__ inline int vmeta_index(int t, int g) {  // half index within scale / offset
+  return ((((t & 7) >> 1) * 8 + g) * 4) + (t & 1) + 2 * (t >> 3);
+}
 
 // Tier-2 keys are stored per 16-token block in mma.m16n8k16 (fp16) A-fragment
 // order, so the original-key scores of a block are 8 tensor-core MMAs fed by
 // one coalesced 16-byte load per lane per k-tile: element (t, c) of a block
 // sits at half index  kt*256 + lane*8 + reg*2 + (cc&1)  with kt = c/16,
-// cc = c%16, lane = (t%8)*4 + (cc%8)/2, reg = t/8 + 2*(cc/8).  Tier-2 values
-// keep the natural [token][channel] order.
+// cc = c%16, lane = (t%8)*4 + (cc%8)/2, reg = t/8 + 2*(cc/8).
 __host__ __device__ inline int k2_offset(int t, int c) {
   int kt = c >> 4, cc = c & 15;
   int lane = (t & 7) * 4 + ((cc & 7) >> 1);
   int reg = (t >> 3) + 2 * (cc >> 3);
   return kt * 256 + lane * 8 + reg * 2 + (cc & 1);
+}
+// Tier-2 values likewise, as the A operand of V^T (rows = channels of group
+// g = c/16, k = tokens): P.V of a block is 8 MMAs with one 16-byte load per
+// lane per group.  Half index g*256 + lane*8 + reg*2 + (t&1), lane =
+// (r%8)*4 + (t%8)/2, reg = r/8 + 2*(t/8), r = c%16.
+__host__ __device__ inline int v2_offset(int t, int c) {
+  int g = c >> 4, r = c & 15;
+  int lane = (r & 7) * 4 + ((t & 7) >> 1);
+  int reg = (r >> 3) + 2 * (t >> 3);
+  return g * 256 + lane * 8 + reg * 2 + (t & 1);
 }
 
 // LRU ring size for a scratch of `cap` blocks (0 = no eviction possible); see scratch.cu
@@ -184,6 +209,44 @@ __device__ __forceinline__ void mma_f16(float (&d)[4], const uint4& a, uint32_t 
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void mma_f16r(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ---- half2 arithmetic on raw 32-bit registers ------------------------------------
+__device__ __forceinline__ uint32_t h2_mul(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t h2_sub(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// pack two floats (lo -> low half) to fp16x2, round to nearest even
+__device__ __forceinline__ uint32_t f2_to_h2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// hi/lo fp16 split of a float pair: x ~= hi + lo to ~22 significant bits
+__device__ __forceinline__ void split_h2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  hi = f2_to_h2(x0, x1);
+  const __half2 h = *reinterpret_cast<const __half2*>(&hi);
+  lo = f2_to_h2(x0 - __low2float(h), x1 - __high2float(h));
 }
 
 // exp via the MUFU ex2 unit (flush-to-zero, rel. error ~2^-22) with a pre-scaled argument

@@ -32,11 +32,67 @@ struct PassASmem {
   uint8_t stage[PA_WARPS][PA_STAGES][REC];
   uint64_t bar[PA_WARPS][PA_STAGES];
   float qh[H * D];
-  float pbuf[PA_WARPS][B][H];
-  float abuf[PA_WARPS][H];
+  float pbuf[PA_WARPS][H][B];  // p' of the block, tokens permuted (vmeta order)
 };
 
-__global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
+// The speculative Phase-2 P.V of one block on the tensor cores.  The INT4
+// codes are fed as fp16 *subnormals* (the bit pattern of the code u is the
+// half u * 2^-24, so one AND per two codes builds the A operand, no bias);
+// B = p' * scale per (token, group) as an fp16 hi/lo pair (column 2h + part),
+// so each product is exact and the sum is fp32.  Tokens 8..15 enter as 16u
+// (nibble at bits 4..7) with their B divided by 16.  The offsets add
+// sum_t p'_t offset_t,g through one more MMA (rows = groups).
+//   acc[g]: rows = channels 16g + l/4 (+8), cols = (head l%4, hi|lo), in
+//           units of 2^(S-24);  accz: rows = groups, same cols, units 2^S.
+struct PVFrag {
+  uint32_t phi0, phi1;   // p' hi of tokens (2j, 2j+1), (2j+8, 2j+9)/16   [column head]
+  uint32_t nph0, nph1;   // -phi on lo-part lanes, 0 on hi lanes
+  uint32_t plo0, plo1;   // p' lo (/16 for the second) on lo lanes, 0 on hi lanes
+  uint32_t z0, z1;       // offset-MMA B: p' hi (hi lanes) or lo (lo lanes), unscaled
+};
+
+__device__ __forceinline__ void pv_frag(PVFrag& F, const float4 p, bool lo_lane) {
+  uint32_t h01, l01, h23, l23;
+  split_h2(p.x, p.y, h01, l01);
+  split_h2(p.z, p.w, h23, l23);
+  F.z0 = lo_lane ? l01 : h01;
+  F.z1 = lo_lane ? l23 : h23;
+  const uint32_t s16 = 0x2c002c00u;  // half2(1/16, 1/16)
+  const uint32_t h23s = h2_mul(h23, s16), l23s = h2_mul(l23, s16);
+  F.phi0 = h01;
+  F.phi1 = h23s;
+  F.nph0 = lo_lane ? (h01 ^ 0x80008000u) : 0u;
+  F.nph1 = lo_lane ? (h23s ^ 0x80008000u) : 0u;
+  F.plo0 = lo_lane ? l01 : 0u;
+  F.plo1 = lo_lane ? l23s : 0u;
+}
+
+__device__ __forceinline__ void pv_block_sub(float (&acc)[NG][4], float (&accz)[4], const PVFrag& F,
+                                            const uint8_t* rec, int lane) {
+  const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+  const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+  const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  const uint4* sc = reinterpret_cast<const uint4*>(rec + OFF_VSCALE + (lane & 3) * 64);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 s4 = sc[q];  // groups 2q, 2q+1: (s_2j, s_2j+1), (s_2j+8, s_2j+9)
+    const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int g = 2 * q + e;
+      const uint32_t s01 = sv[2 * e], s23 = sv[2 * e + 1];
+      const uint32_t b0 = h2_fma(F.plo0, s01, h2_fma(F.phi0, s01, h2_mul(F.nph0, s01)));
+      const uint32_t b1 = h2_fma(F.plo1, s23, h2_fma(F.phi1, s23, h2_mul(F.nph1, s23)));
+      const uint32_t w = wv[(g >> 2) * 4 + (g & 3)];
+      const uint32_t w8 = w >> 8;
+      mma_f16r(acc[g], w & 0x000f000fu, w8 & 0x000f000fu, w & 0x00f000f0u, w8 & 0x00f000f0u, b0, b1);
+    }
+  }
+  const uint2 oz = *reinterpret_cast<const uint2*>(rec + OFF_VOFF + ((lane & 3) * 8 + (lane >> 2)) * 8);
+  mma_f16r(accz, oz.x, 0u, oz.y, 0u, F.z0, F.z1);
+}
+
+__global__ void __launch_bounds__(PA_WARPS * 32, 3) k_pass_a(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;
@@ -47,7 +103,6 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
   const int nb = c.n_blocks[u];
   const int b0 = sp * st.blocks_per_split;
   const int b1 = min(nb, b0 + st.blocks_per_split);
-  const float inv_sqrt_d = 0.08838834764831845f;
 
   for (int i = tid; i < H * D; i += blockDim.x) {
     int h = i / D;
@@ -60,7 +115,6 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-  (void)inv_sqrt_d;
 
   QFrag f;
   load_qfrag(f, S.qh, lane);
@@ -79,13 +133,19 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
 
   const int h = lane & 3;
   const int t0 = lane >> 2, t1 = t0 + 8;
+  const int pi0 = 4 * (t0 >> 1) + (t0 & 1);  // permuted positions of t0, t1
+  const int pi1 = pi0 + 2;
+  const int hb = lane >> 3;                  // head of this lane's B column
+  const bool lo_lane = (lane >> 2) & 1;
+  const int Sx = value_exp(c.v_max[u]);
+  const float p2S = pow2f(Sx);
   float m_run = ninf(), l_run = 0.f, dmax = 0.f;
-  float2 o2[H][2];
+  float acc[NG][4], accz[4];
 #pragma unroll
-  for (int i = 0; i < H; ++i) o2[i][0] = o2[i][1] = make_float2(0.f, 0.f);
+  for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+  accz[0] = accz[1] = accz[2] = accz[3] = 0.f;
 
   float* lm1 = st.lm1 + ((size_t)u * nh + (h < nh ? h : 0)) * c.max_blocks;
-  const int g = lane >> 2;  // value group of the lane's channels
 
   for (int i = 0; i < nmine; ++i) {
     const int s = i % PA_STAGES;
@@ -110,60 +170,25 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
     dmax = fmaxf(dmax, r.delta);
     const float m_new = fmaxf(m_run, bm);
     const float alpha = fast_exp(m_run - m_new);
-    const float beta = fast_exp(bm - m_new);
+    const float beta = fast_exp(bm - m_new) * p2S;
     l_run = l_run * alpha + bs * beta;
     m_run = m_new;
-    S.pbuf[warp][t0][h] = e0 * beta;
-    S.pbuf[warp][t1][h] = e1 * beta;
-    if (lane < H) S.abuf[warp][lane] = alpha;
+    S.pbuf[warp][h][pi0] = e0 * beta;
+    S.pbuf[warp][h][pi1] = e1 * beta;
+    // rescale this lane's accumulators (all belong to head l%4)
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        acc[g][0] *= alpha; acc[g][1] *= alpha; acc[g][2] *= alpha; acc[g][3] *= alpha;
+      }
+      accz[0] *= alpha; accz[1] *= alpha; accz[2] *= alpha; accz[3] *= alpha;
+    }
     __syncwarp();
 
-    // ---- speculative phase 2: INT4 values, lane owns channels 4l..4l+3 --------
-    // packed fp32x2 FMAs (FFMA2): channel pairs (0,1) and (2,3)
-    if (__any_sync(0xffffffffu, alpha != 1.f)) {
-      const float4 al = *reinterpret_cast<const float4*>(S.abuf[warp]);
-      const float alv[4] = {al.x, al.y, al.z, al.w};
-#pragma unroll
-      for (int hh = 0; hh < H; ++hh) {
-        const float2 a2 = make_float2(alv[hh], alv[hh]);
-        o2[hh][0] = __fmul2_rn(o2[hh][0], a2);
-        o2[hh][1] = __fmul2_rn(o2[hh][1], a2);
-      }
-    }
-    const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
-    const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
-    const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const uint4* vm = reinterpret_cast<const uint4*>(rec + OFF_VMETA + g * 64);
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
-      const uint4 mm = vm[q4];
-      const uint32_t mv[4] = {mm.x, mm.y, mm.z, mm.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int t = q4 * 4 + k;
-        const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
-        const __half2 so = *reinterpret_cast<const __half2*>(&mv[k]);
-        const float2 sof = __half22float2(so);
-        // v = u*s + o = (16 + u)*s + (o - 16 s); 16 + u is the float with
-        // exponent 4 and the nibble in the top mantissa bits
-        const float op = fmaf(-16.f, sof.x, sof.y);
-        float fb[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          fb[j] = __uint_as_float(((cw << (19 - 4 * j)) & 0x00780000u) | 0x41800000u);
-        const float2 s2 = make_float2(sof.x, sof.x), o2c = make_float2(op, op);
-        const float2 v01 = __ffma2_rn(make_float2(fb[0], fb[1]), s2, o2c);
-        const float2 v23 = __ffma2_rn(make_float2(fb[2], fb[3]), s2, o2c);
-        const float4 p4 = *reinterpret_cast<const float4*>(S.pbuf[warp][t]);
-        const float pv[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-        for (int hh = 0; hh < H; ++hh) {
-          const float2 pp = make_float2(pv[hh], pv[hh]);
-          o2[hh][0] = __ffma2_rn(pp, v01, o2[hh][0]);
-          o2[hh][1] = __ffma2_rn(pp, v23, o2[hh][1]);
-        }
-      }
-    }
+    // ---- speculative phase 2 on the tensor cores -----------------------------
+    PVFrag F;
+    pv_frag(F, *reinterpret_cast<const float4*>(&S.pbuf[warp][hb][4 * (lane & 3)]), lo_lane);
+    pv_block_sub(acc, accz, F, rec, lane);
     __syncwarp();
     if (lane == 0 && i + PA_STAGES < nmine) {
       fence_proxy_async();
@@ -173,21 +198,24 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
     }
   }
 
+  // ---- per-lane outputs: O[c][h] = (acc * 2^24 + offset sum) * 2^-S ----------
+  const float oz = accz[0] + accz[1];  // group l/4, head l%4
+  const float inv = pow2f(-Sx);
   // ---- merge the four warps of the CTA, write the split state ---------------
   __syncthreads();
   float* mw = reinterpret_cast<float*>(S.stage);        // [warp][h][4]: m, l, dmax
   float* ow = mw + PA_WARPS * H * 4;                     // [warp][h][D]
   if (lane < H) {
     mw[(warp * H + lane) * 4 + 0] = m_run;
-    mw[(warp * H + lane) * 4 + 1] = l_run;
+    mw[(warp * H + lane) * 4 + 1] = l_run * inv;
     mw[(warp * H + lane) * 4 + 2] = dmax;
   }
 #pragma unroll
-  for (int hh = 0; hh < H; ++hh) {
-    ow[(warp * H + hh) * D + lane * 4 + 0] = o2[hh][0].x;
-    ow[(warp * H + hh) * D + lane * 4 + 1] = o2[hh][0].y;
-    ow[(warp * H + hh) * D + lane * 4 + 2] = o2[hh][1].x;
-    ow[(warp * H + hh) * D + lane * 4 + 3] = o2[hh][1].y;
+  for (int g = 0; g < NG; ++g) {
+    const float zg = __shfl_sync(0xffffffffu, oz, 4 * g + h);
+    const int c0 = 16 * g + t0;
+    ow[(warp * H + h) * D + c0] = fmaf(acc[g][0] + acc[g][1], 16777216.f, zg) * inv;
+    ow[(warp * H + h) * D + c0 + 8] = fmaf(acc[g][2] + acc[g][3], 16777216.f, zg) * inv;
   }
   __syncthreads();
   const int ch = tid;  // 128 threads = 128 channels

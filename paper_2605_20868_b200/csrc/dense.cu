@@ -55,15 +55,15 @@ __global__ void k_resolve(DenseArgs a) {
 
 struct DenseSmem {
   float qh[H * D];
-  float w[DN_WARPS][B][H];
-  float al[DN_WARPS][H];
+  float w[DN_WARPS][H][B];  // softmax weights x 2^14, tokens permuted (B-fragment order)
 };
 
 // Exact attention over the full blocks of one split of a flagged unit; all
 // four q-heads share every K/V read.  Scores come from orig_block (FP16 keys
-// x hi/lo-split q' on the tensor cores, fp32 accumulate); the softmax and the
-// value accumulation run in fp32.  The partial block is added in k_dense_merge
-// from the state k_select already computed for it.
+// x hi/lo-split q' on the tensor cores, fp32 accumulate); P.V runs on the
+// tensor cores too: A = the fragment-ordered FP16 values (exact), B = the
+// weights as an fp16 hi/lo pair (column 2h + part), fp32 accumulation.  The
+// partial block is added in k_dense_merge from the state k_select computed.
 __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   __shared__ DenseSmem S;
   __shared__ float ow[DN_WARPS][H][D];
@@ -94,12 +94,19 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   QFrag16 f16;
   load_qfrag16(f16, S.qh, lane);
   const int h = lane & 3, t0 = lane >> 2;
+  const int pi0 = 4 * (t0 >> 1) + (t0 & 1), pi1 = pi0 + 2;
+  const int hb = lane >> 3;
+  const bool lo_lane = (lane >> 2) & 1;
   const size_t ubk = (size_t)u * c.max_blocks;
   float m_h = dninf(), l_h = 0.f;
-  float2 acc[H][2];
+  float acc[NG][4];
 #pragma unroll
-  for (int i = 0; i < H; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
   for (int b = b0 + warp; b < b1; b += DN_WARPS) {
+    const uint4* vf = reinterpret_cast<const uint4*>(c.tier2_v + (ubk + b) * B * D);
+    uint4 av[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
     const float2 s = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
     float bmx = fmaxf(s.x, s.y);
     bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 4));
@@ -110,31 +117,22 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
     m_h = m_new;
     const float w0 = expf(s.x - m_h), w1 = expf(s.y - m_h);
     l_h = l_h * alpha + w0 + w1;
-    S.w[warp][t0][h] = w0;
-    S.w[warp][t0 + 8][h] = w1;
-    if (lane < H) S.al[warp][lane] = alpha;
-    __syncwarp();
-    const float4 al4 = *reinterpret_cast<const float4*>(S.al[warp]);
-    const float alv[4] = {al4.x, al4.y, al4.z, al4.w};
+    S.w[warp][h][pi0] = w0 * 16384.f;
+    S.w[warp][h][pi1] = w1 * 16384.f;
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-    for (int hh = 0; hh < H; ++hh) {
-      acc[hh][0] = __fmul2_rn(acc[hh][0], make_float2(alv[hh], alv[hh]));
-      acc[hh][1] = __fmul2_rn(acc[hh][1], make_float2(alv[hh], alv[hh]));
-    }
-    const uint16_t* vp = c.tier2_v + (ubk + b) * B * D + lane * 4;
-#pragma unroll 4
-    for (int t = 0; t < B; ++t) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(vp + (size_t)t * D);
-      const float2 v01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-      const float2 v23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-      const float4 w4 = *reinterpret_cast<const float4*>(S.w[warp][t]);
-      const float wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-      for (int hh = 0; hh < H; ++hh) {
-        acc[hh][0] = __ffma2_rn(make_float2(wv[hh], wv[hh]), v01, acc[hh][0]);
-        acc[hh][1] = __ffma2_rn(make_float2(wv[hh], wv[hh]), v23, acc[hh][1]);
+      for (int g = 0; g < NG; ++g) {
+        acc[g][0] *= alpha; acc[g][1] *= alpha; acc[g][2] *= alpha; acc[g][3] *= alpha;
       }
     }
+    __syncwarp();
+    uint32_t h01, l01, h23, l23;
+    const float4 p4 = *reinterpret_cast<const float4*>(&S.w[warp][hb][4 * (lane & 3)]);
+    split_h2(p4.x, p4.y, h01, l01);
+    split_h2(p4.z, p4.w, h23, l23);
+    const uint32_t bb0 = lo_lane ? l01 : h01, bb1 = lo_lane ? l23 : h23;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, bb0, bb1);
     __syncwarp();
   }
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 4);
@@ -145,11 +143,9 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
     mw[warp][lane][1] = l_h;
   }
 #pragma unroll
-  for (int hh = 0; hh < H; ++hh) {
-    ow[warp][hh][lane * 4 + 0] = acc[hh][0].x;
-    ow[warp][hh][lane * 4 + 1] = acc[hh][0].y;
-    ow[warp][hh][lane * 4 + 2] = acc[hh][1].x;
-    ow[warp][hh][lane * 4 + 3] = acc[hh][1].y;
+  for (int g = 0; g < NG; ++g) {
+    ow[warp][h][16 * g + t0] = (acc[g][0] + acc[g][1]) * (1.f / 16384.f);
+    ow[warp][h][16 * g + t0 + 8] = (acc[g][2] + acc[g][3]) * (1.f / 16384.f);
   }
   __syncthreads();
   for (int hh = 0; hh < H; ++hh) {

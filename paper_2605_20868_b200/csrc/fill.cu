@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
   __shared__ uint16_t sv[B][D];
   __shared__ double sq[B][D];   // squared reconstruction error, then reused
   __shared__ double sn[B][D];   // squared value
+  __shared__ uint8_t vcs[B][D]; // value codes, unpacked
   __shared__ float red[4];
 
   // ---- gather the 16 tokens of this block from [partial | new] -------------
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
     kx[t] = half_bits_to_double(kb);
     sv[t][tid] = vb;
     c.tier2_k[t2base + k2_offset(t, tid)] = kb;
-    c.tier2_v[t2base + t * D + tid] = vb;
+    c.tier2_v[t2base + v2_offset(t, tid)] = vb;
   }
 
   // ---- keys: thread = channel (quantizer.py:133-150) ----------------------
@@ -151,14 +152,26 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
       sn[t][g * G + i] = __dmul_rn(v[i], v[i]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // lanes 4g+q hold channels 16g+4q .. +3
-      uint16_t w = (uint16_t)(nib[4 * q] | (nib[4 * q + 1] << 4) | (nib[4 * q + 2] << 8) |
-                              (nib[4 * q + 3] << 12));
-      int l = 4 * g + q;
-      *reinterpret_cast<uint16_t*>(rec + OFF_VCODES + (t >> 3) * 512 + l * 16 + (t & 7) * 2) = w;
+    for (int i = 0; i < G; ++i) vcs[t][g * G + i] = (uint8_t)nib[i];
+    reinterpret_cast<uint16_t*>(rec + OFF_VSCALE)[vmeta_index(t, g)] = s16;
+    reinterpret_cast<uint16_t*>(rec + OFF_VOFF)[vmeta_index(t, g)] = o16;
+  }
+  __syncthreads();
+  // pack the nibbles in fragment order (common.cuh): 256 words, two per thread
+  for (int wi = tid; wi < 256; wi += 128) {
+    const int g = (wi >> 7) * 4 + (wi & 3), l = (wi >> 2) & 31;
+    const int r = l >> 2, j = l & 3;
+    uint32_t w = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = 2 * j + (k & 1) + 8 * (k >> 1);
+#pragma unroll
+      for (int up = 0; up < 2; ++up) {
+        const int ch = 16 * g + r + 8 * up;
+        w |= (uint32_t)vcs[t][ch] << vcode_bit(t, ch);
+      }
     }
-    uint32_t meta = (uint32_t)s16 | ((uint32_t)o16 << 16);
-    *reinterpret_cast<uint32_t*>(rec + vmeta_offset(t, g)) = meta;
+    *reinterpret_cast<uint32_t*>(rec + OFF_VCODES + wi * 4) = w;
   }
   __syncthreads();
 
@@ -219,18 +232,15 @@ __global__ void k_read_tier1(ckv_cache c, int u, int b0, int8_t* kc, float* ks, 
   const uint8_t* rec = c.tier1 + ((size_t)u * c.max_blocks + b0 + i) * REC;
   for (int t = 0; t < B; ++t) {
     kc[((size_t)i * B + t) * D + tid] = (int8_t)rec[kcode_offset(t, tid)];
-    uint8_t byte = rec[vcode_offset(t, tid)];
-    // channel 4l+j sits at bits 4j of the u16; byte index picks j>>1
-    int j = tid & 3;
-    vc[((size_t)i * B + t) * D + tid] = (byte >> ((j & 1) * 4)) & 0xF;
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(rec + vcode_word(t, tid));
+    vc[((size_t)i * B + t) * D + tid] = (uint8_t)((w >> vcode_bit(t, tid)) & 0xFu);
   }
   ks[(size_t)i * D + tid] = reinterpret_cast<const float*>(rec + OFF_KSCALE)[tid];
   ko[(size_t)i * D + tid] = reinterpret_cast<const float*>(rec + OFF_KOFF)[tid];
   {
     int t = tid >> 3, g = tid & 7;
-    uint32_t m = *reinterpret_cast<const uint32_t*>(rec + vmeta_offset(t, g));
-    vs[((size_t)i * B + t) * NG + g] = (uint16_t)(m & 0xffff);
-    vo[((size_t)i * B + t) * NG + g] = (uint16_t)(m >> 16);
+    vs[((size_t)i * B + t) * NG + g] = reinterpret_cast<const uint16_t*>(rec + OFF_VSCALE)[vmeta_index(t, g)];
+    vo[((size_t)i * B + t) * NG + g] = reinterpret_cast<const uint16_t*>(rec + OFF_VOFF)[vmeta_index(t, g)];
   }
 }
 

@@ -88,30 +88,42 @@ __global__ void __launch_bounds__(UN_THREADS) k_union(StepArgs a) {
 
 // -----------------------------------------------------------------------------
 constexpr int PB_WARPS = 4;
-constexpr int PB_IPC = 32;  // work items per chunk
 
 struct PassBSmem {
   uint8_t rec[PB_WARPS][2][REC];
   uint8_t kt[PB_WARPS][2][B * D * 2];  // FP16 Tier-2 key tile (fragment order) of promoted blocks
   uint64_t bar[PB_WARPS][2];
   float qh[H * D];
-  float wn[PB_WARPS][B][H];
-  float wq[PB_WARPS][B][H];
-  float al[PB_WARPS][H];
+  float cq[PB_WARPS][H][B];  // coefficient of v_hat per (head, token), tokens permuted
+  float ca[PB_WARPS][H][B];  // coefficient of the original v
 };
 
-__global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
+// A operand of the INT4 codes as exact fp16 integers (1024 + u) - 1024 for
+// group g (see the record layout in common.cuh).
+__device__ __forceinline__ void vcode_a(uint32_t w, uint32_t& a0, uint32_t& a1, uint32_t& a2,
+                                        uint32_t& a3) {
+  const uint32_t magic = 0x64006400u, m1024 = 0x64006400u;
+  const uint32_t k16 = 0x2c002c00u, m64 = 0xd400d400u;  // 1/16, -64
+  const uint32_t w8 = w >> 8;
+  a0 = h2_sub((w & 0x000f000fu) | magic, m1024);
+  a1 = h2_sub((w8 & 0x000f000fu) | magic, m1024);
+  a2 = h2_fma((w & 0x00f000f0u) | magic, k16, m64);   // (1024 + 16u) / 16 - 64
+  a3 = h2_fma((w8 & 0x00f000f0u) | magic, k16, m64);
+}
+
+__global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int ck = blockIdx.x, u = blockIdx.y;
   const int C = gridDim.x;
+  const int IPC = st.items_per_chunk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
   const int nwork = st.n_work[u];
   float* cs = st.chunk_state + ((size_t)u * C + ck) * H * CKV_CHUNK_FLOATS;
-  if (ck * PB_IPC >= nwork) {
+  if (ck * IPC >= nwork) {
     if (tid < H) cs[tid * CKV_CHUNK_FLOATS] = ninf();
     return;
   }
@@ -142,23 +154,28 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
   if (m_h == ninf()) m_h = -1e30f;
   float dden = 0.f, canary = 0.f;
   double eF = 0.0, sF = 0.0;
-  float2 acc[H][2];
+  float acc[NG][4], accz[4];
 #pragma unroll
-  for (int i = 0; i < H; ++i) acc[i][0] = acc[i][1] = make_float2(0.f, 0.f);
+  for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+  accz[0] = accz[1] = accz[2] = accz[3] = 0.f;
+  const int Sx = value_exp(c.v_max[u]);
+  const float p2S = pow2f(Sx);
 
   const size_t ubk = (size_t)u * c.max_blocks;
   const int32_t* work = st.work + (size_t)u * st.wcap;
   const float* eta = c.eta + ubk;
   float* lm2 = st.lm2 + ((size_t)u * nh + hq) * c.max_blocks;
-  const int g = lane >> 2;
   const int t0 = lane >> 2;
+  const int pi0 = 4 * (t0 >> 1) + (t0 & 1), pi1 = pi0 + 2;
+  const int hb = lane >> 3;
+  const bool lo_lane = (lane >> 2) & 1;
 
   // this warp's item sequence: chunks ck, ck+C, ...; items base+warp, +4, ...
   auto item_at = [&](int k) -> int {  // k-th item of this warp, or -1
-    const int per_chunk = (PB_IPC + PB_WARPS - 1 - warp) / PB_WARPS;
+    const int per_chunk = (IPC + PB_WARPS - 1 - warp) / PB_WARPS;
     const int chunk = k / per_chunk, within = k % per_chunk;
-    const int idx = (ck + chunk * C) * PB_IPC + warp + within * PB_WARPS;
-    const int cend = min(nwork, (ck + chunk * C) * PB_IPC + PB_IPC);
+    const int idx = (ck + chunk * C) * IPC + warp + within * PB_WARPS;
+    const int cend = min(nwork, (ck + chunk * C) * IPC + IPC);
     return (idx < cend) ? idx : -1;
   };
   const uint8_t* t1base = c.tier1 + ubk * REC;
@@ -236,65 +253,64 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
         }
       }
     }
-    // branch-free correction coefficients: acc_h += a * v_orig + c * v_hat
-    //   F & V: a = wn, c = -wq   F only: a = 0, c = wn - wq
-    //   V only: a = wq, c = -wq  neither: a = c = 0
-    S.wn[warp][t0][h] = inV ? (inF ? wn0 : wq0) : 0.f;
-    S.wn[warp][t0 + 8][h] = inV ? (inF ? wn1 : wq1) : 0.f;
-    S.wq[warp][t0][h] = inV ? -wq0 : (inF ? wn0 - wq0 : 0.f);
-    S.wq[warp][t0 + 8][h] = inV ? -wq1 : (inF ? wn1 - wq1 : 0.f);
-    if (lane < H) S.al[warp][lane] = alpha;
-    __syncwarp();
-    {
-      const float4 al4 = *reinterpret_cast<const float4*>(S.al[warp]);
-      const float alv[4] = {al4.x, al4.y, al4.z, al4.w};
+    // branch-free correction coefficients: acc_h += ca * v_orig + cq * v_hat
+    //   F & V: ca = wn, cq = -wq   F only: ca = 0, cq = wn - wq
+    //   V only: ca = wq, cq = -wq  neither: ca = cq = 0
+    S.ca[warp][h][pi0] = (inV ? (inF ? wn0 : wq0) : 0.f) * p2S;
+    S.ca[warp][h][pi1] = (inV ? (inF ? wn1 : wq1) : 0.f) * p2S;
+    S.cq[warp][h][pi0] = (inV ? -wq0 : (inF ? wn0 - wq0 : 0.f)) * p2S;
+    S.cq[warp][h][pi1] = (inV ? -wq1 : (inF ? wn1 - wq1 : 0.f)) * p2S;
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-      for (int hh = 0; hh < H; ++hh) {
-        acc[hh][0] = __fmul2_rn(acc[hh][0], make_float2(alv[hh], alv[hh]));
-        acc[hh][1] = __fmul2_rn(acc[hh][1], make_float2(alv[hh], alv[hh]));
+      for (int g = 0; g < NG; ++g) {
+        acc[g][0] *= alpha; acc[g][1] *= alpha; acc[g][2] *= alpha; acc[g][3] *= alpha;
       }
+      accz[0] *= alpha; accz[1] *= alpha; accz[2] *= alpha; accz[3] *= alpha;
     }
-    // values: lane owns channels 4*lane .. 4*lane+3
-    const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
-    const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
-    const uint32_t cw2[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const uint32_t* vmeta = reinterpret_cast<const uint32_t*>(rec + OFF_VMETA + g * 64);
-    const int vsl = (vm && vslot) ? vslot[b] : -1;
-    const uint16_t* vorig = ((vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D
-                                        : c.tier2_v + (ubk + b) * B * D) + lane * 4;
-#pragma unroll 4
-    for (int t = 0; t < B; ++t) {
-      const uint32_t cw = (cw2[t >> 1] >> ((t & 1) * 16)) & 0xffffu;
-      const uint32_t mm = vmeta[t];
-      const float2 sof = __half22float2(*reinterpret_cast<const __half2*>(&mm));
-      const float op = fmaf(-16.f, sof.x, sof.y);
-      float fbv[4];
+    __syncwarp();
+    {  // v_hat part: B = cq' * scale per group (hi/lo), exact integer codes
+      uint32_t h01, l01, h23, l23;
+      const float4 p4 = *reinterpret_cast<const float4*>(&S.cq[warp][hb][4 * (lane & 3)]);
+      split_h2(p4.x, p4.y, h01, l01);
+      split_h2(p4.z, p4.w, h23, l23);
+      const uint32_t nph0 = lo_lane ? (h01 ^ 0x80008000u) : 0u, nph1 = lo_lane ? (h23 ^ 0x80008000u) : 0u;
+      const uint32_t plo0 = lo_lane ? l01 : 0u, plo1 = lo_lane ? l23 : 0u;
+      const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+      const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+      const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+      const uint4* sc = reinterpret_cast<const uint4*>(rec + OFF_VSCALE + (lane & 3) * 64);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        fbv[j] = __uint_as_float(((cw << (19 - 4 * j)) & 0x00780000u) | 0x41800000u);
-      const float2 vq01 = __ffma2_rn(make_float2(fbv[0], fbv[1]), make_float2(sof.x, sof.x),
-                                     make_float2(op, op));
-      const float2 vq23 = __ffma2_rn(make_float2(fbv[2], fbv[3]), make_float2(sof.x, sof.x),
-                                     make_float2(op, op));
-      const float4 a4 = *reinterpret_cast<const float4*>(S.wn[warp][t]);
-      const float4 c4 = *reinterpret_cast<const float4*>(S.wq[warp][t]);
-      const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-      const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+      for (int q = 0; q < 4; ++q) {
+        const uint4 s4 = sc[q];
+        const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-      for (int hh = 0; hh < H; ++hh) {
-        acc[hh][0] = __ffma2_rn(make_float2(cv[hh], cv[hh]), vq01, acc[hh][0]);
-        acc[hh][1] = __ffma2_rn(make_float2(cv[hh], cv[hh]), vq23, acc[hh][1]);
-      }
-      if (vm) {  // warp-uniform: some head of this block is value-promoted
-        const uint2 raw = *reinterpret_cast<const uint2*>(vorig + (size_t)t * D);
-        const float2 vo01 = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
-        const float2 vo23 = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
-#pragma unroll
-        for (int hh = 0; hh < H; ++hh) {
-          acc[hh][0] = __ffma2_rn(make_float2(av[hh], av[hh]), vo01, acc[hh][0]);
-          acc[hh][1] = __ffma2_rn(make_float2(av[hh], av[hh]), vo23, acc[hh][1]);
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int g = 2 * q + e2;
+          const uint32_t s01 = sv[2 * e2], s23 = sv[2 * e2 + 1];
+          const uint32_t b0 = h2_fma(plo0, s01, h2_fma(h01, s01, h2_mul(nph0, s01)));
+          const uint32_t b1 = h2_fma(plo1, s23, h2_fma(h23, s23, h2_mul(nph1, s23)));
+          uint32_t a0, a1, a2, a3;
+          vcode_a(wv[g], a0, a1, a2, a3);
+          mma_f16r(acc[g], a0, a1, a2, a3, b0, b1);
         }
       }
+      const uint2 oz = *reinterpret_cast<const uint2*>(rec + OFF_VOFF + ((lane & 3) * 8 + (lane >> 2)) * 8);
+      mma_f16r(accz, oz.x, 0u, oz.y, 0u, lo_lane ? l01 : h01, lo_lane ? l23 : h23);
+    }
+    if (vm) {  // warp-uniform: some head of this block is value-promoted: B = ca' (hi/lo)
+      uint32_t h01, l01, h23, l23;
+      const float4 p4 = *reinterpret_cast<const float4*>(&S.ca[warp][hb][4 * (lane & 3)]);
+      split_h2(p4.x, p4.y, h01, l01);
+      split_h2(p4.z, p4.w, h23, l23);
+      const uint32_t b0 = lo_lane ? l01 : h01, b1 = lo_lane ? l23 : h23;
+      const int vsl = vslot ? vslot[b] : -1;
+      const uint4* vf = reinterpret_cast<const uint4*>(
+          (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
+      uint4 av[NG];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
+#pragma unroll
+      for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, b0, b1);
     }
     __syncwarp();
     cur = nxt;
@@ -307,17 +323,18 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) k_pass_b(StepArgs a) {
   canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 4));
   canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 8));
   canary = fmaxf(canary, __shfl_xor_sync(0xffffffffu, canary, 16));
+  const float oz = accz[0] + accz[1];
+  const float inv = pow2f(-Sx);
   __syncthreads();
   float* accs = reinterpret_cast<float*>(S.rec);             // [warp][H][D]
   float* mw = accs + PB_WARPS * H * D;                        // [warp][H][4]
   double* dw = reinterpret_cast<double*>(mw + PB_WARPS * H * 4);  // [warp][H][2]
 #pragma unroll
-  for (int hh = 0; hh < H; ++hh) {
-    float* p = accs + (warp * H + hh) * D + lane * 4;
-    p[0] = acc[hh][0].x;
-    p[1] = acc[hh][0].y;
-    p[2] = acc[hh][1].x;
-    p[3] = acc[hh][1].y;
+  for (int g = 0; g < NG; ++g) {
+    const float zg = __shfl_sync(0xffffffffu, oz, 4 * g + h);
+    const int c0 = 16 * g + t0;
+    accs[(warp * H + h) * D + c0] = (acc[g][0] + acc[g][1] + zg) * inv;
+    accs[(warp * H + h) * D + c0 + 8] = (acc[g][2] + acc[g][3] + zg) * inv;
   }
   if (lane < H) {
     mw[(warp * H + lane) * 4 + 0] = m_h;

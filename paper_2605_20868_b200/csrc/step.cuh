@@ -42,6 +42,14 @@ struct StepArgs {
   PageView pv;
 };
 
+// Exponent S of the unit's value scaling: every fp16 product p' * scale with
+// p' = p * 2^S <= 2^S stays below 2^15 (scale <= max(2 v_max / 15, 1), since
+// |v| <= nu <= v_max and a constant group has scale 1).
+__device__ __forceinline__ int value_exp(float vmax) {
+  const float sb = fmaxf(2.f * vmax * (1.f / 15.f), 1.f);
+  return 14 - (ilogbf(sb) + 1);
+}
+
 __device__ __forceinline__ float ninf() { return __int_as_float(0xff800000); }
 
 __device__ __forceinline__ uint32_t okey(float x) {  // order-preserving float -> u32
