@@ -92,7 +92,7 @@ __device__ __forceinline__ void pv_block_sub(float (&acc)[NG][4], float (&accz)[
   mma_f16r(accz, oz.x, 0u, oz.y, 0u, F.z0, F.z1);
 }
 
-__global__ void __launch_bounds__(PA_WARPS * 32, 3) k_pass_a(StepArgs a) {
+__global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;
@@ -132,8 +132,8 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 3) k_pass_a(StepArgs a) {
   }
 
   const int h = lane & 3;
-  const int t0 = lane >> 2, t1 = t0 + 8;
-  const int pi0 = 4 * (t0 >> 1) + (t0 & 1);  // permuted positions of t0, t1
+  const int t0 = lane >> 2;
+  const int pi0 = 4 * (t0 >> 1) + (t0 & 1);  // permuted positions of tokens t0, t0 + 8
   const int pi1 = pi0 + 2;
   const int hb = lane >> 3;                  // head of this lane's B column
   const bool lo_lane = (lane >> 2) & 1;
@@ -147,11 +147,13 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 3) k_pass_a(StepArgs a) {
 
   float* lm1 = st.lm1 + ((size_t)u * nh + (h < nh ? h : 0)) * c.max_blocks;
 
+  float smax_nxt = (nmine > 0) ? __ldg(smax_u + b0 + warp) : 0.f;
   for (int i = 0; i < nmine; ++i) {
     const int s = i % PA_STAGES;
     const uint32_t par = (uint32_t)(i / PA_STAGES) & 1u;
     const int b = b0 + warp + PA_WARPS * i;
-    const float smax = __ldg(smax_u + b);
+    const float smax = smax_nxt;  // loaded one iteration ahead
+    if (i + 1 < nmine) smax_nxt = __ldg(smax_u + b + PA_WARPS);
     mbar_wait(&S.bar[warp][s], par);
     const uint8_t* rec = S.stage[warp][s];
 

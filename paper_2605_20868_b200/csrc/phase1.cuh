@@ -20,7 +20,7 @@ namespace ckv {
 
 struct QFrag {
   float qsc[32];   // q'_{h,c} * 2^(21-eQ_h) for h = lane/8, the lane's 32 channels
-  float aw[32];    // odd (lane/4): qsc (for sum q' z); even: |qsc| (for Delta)
+  uint32_t amask;  // odd (lane/4): all ones (qsc, for sum q' z); even: clears the sign (|qsc|, Delta)
   int eq_l;        // exponent of head lane%4: max|q'_h| < 2^eq_l
 };
 
@@ -49,13 +49,13 @@ __device__ inline void load_qfrag(QFrag& f, const float* qh, int lane) {
   }
   const float sc = pow2f(21 - eq_b);
   const bool odd = (lane >> 2) & 1;
+  f.amask = odd ? 0xffffffffu : 0x7fffffffu;
 #pragma unroll
   for (int kt = 0; kt < 4; ++kt) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float v = qh[hb * D + bchan(lane, kt, j)] * sc;
       f.qsc[kt * 8 + j] = v;
-      f.aw[kt * 8 + j] = odd ? v : fabsf(v);
     }
   }
 }
@@ -94,7 +94,7 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       y[j] = __float_as_uint(fmaf(f.qsc[kt * 8 + j], sv[j], magic_b));
-      acc = fmaf(f.aw[kt * 8 + j], xv[j], acc);
+      acc = fmaf(__uint_as_float(__float_as_uint(f.qsc[kt * 8 + j]) & f.amask), xv[j], acc);
     }
     // tile 0: byte (lane/4)&1 of the four U values, packed into one register
     uint32_t b00 = __byte_perm(__byte_perm(y[0], y[1], sel0), __byte_perm(y[2], y[3], sel0), 0x5410);
