@@ -233,8 +233,13 @@ def main():
     pol = ck.PolicyConfig(exploration_rate=0.0)
     cap = cache.max_blocks if args.scratch < 0 else args.scratch
     scratch = ck.ScratchCache(cap) if args.scratch != 0 else None
+    from paper_2605_20868_b200 import sharding
+    my_units = sharding.shard_units(args.layers, args.kv_heads, args.batch, world, rank)
+    # step-wide Rung 4 per (layer, sequence), shared by the ranks holding that layer's KV heads
+    groups = np.asarray(list(my_units)) % (args.layers * args.batch)
     dec = ck.CertifiedDecoder(cache, pol, n_heads=args.q_per_kv, scratch=scratch,
-                              rung4_group=None)
+                              rung4_group=groups)
+    assert dec.n_groups == args.layers * args.batch
     nq = W + K
     qpool = torch.randn((nq, U, args.q_per_kv, 128), generator=g, device=dev, dtype=torch.float64)
     kpool = torch.randn((nq, U, 1, 128), generator=g, device=dev).half()
@@ -244,43 +249,49 @@ def main():
     for a, b in ev_a:  # torch creates the CUDA event lazily: force it before handing it over
         a.record()
         b.record()
-    from paper_2605_20868_b200 import sharding
-    my_units = sharding.shard_units(args.layers, args.kv_heads, args.batch, world, rank)
-    my_layers = sharding.layer_of_units(my_units, args.layers, args.batch)
 
-    def exchange(res):
-        if world == 1:
-            return
-        # the bound report: outputs + certificates of every rank (one NCCL all-gather),
-        # and the per-layer Rung-4 flag (MAX all-reduce)
-        sharding.gather_bound_report(dec.out, dec.cert_buf)
-        r4 = (res.cert["flags"] & (_lib.F_CANARY | _lib.F_NUMERIC)).any(axis=1)
-        sharding.rung4_layers(r4, my_layers, args.layers, device=dev)
+    reduce_flags = None
+    if world > 1:
+        def reduce_flags(flags):  # per-layer Rung-4 request, MAX over ranks (NCCL, no host sync)
+            dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+
+    def exchange():
+        if world > 1:  # the bound report: outputs + certificates of every rank, one all-gather
+            sharding.gather_bound_report(dec.out, dec.cert_buf)
 
     launches = {"n": 0}
     dense_heads = {"n": 0}
-
     last = {}
+    pending = {"p": None}
+
+    def collect():
+        p = pending["p"]
+        if p is not None:
+            res = p.result()
+            dense_heads["n"] += int((res.kinds != 0).sum())
+            last["res"] = res
+            pending["p"] = None
 
     def one_step(i, timed_ev=None):
+        # the host decodes step i-1's certificates while the device runs step i
         if timed_ev is not None:
             dec.st.prof_begin = timed_ev[0].cuda_event
             dec.st.prof_end = timed_ev[1].cuda_event
-        res = dec.step(qpool[i])
+        p = dec.step_async(qpool[i], reduce_flags)
         dec.st.prof_begin = None
         dec.st.prof_end = None
         launches["n"] += lib.ckv_last_launches()
-        dense_heads["n"] += int((res.kinds != 0).sum())
-        last["res"] = res
-        exchange(res)
+        exchange()
         cache.append(kpool[i], vpool[i], validate=False)
         launches["n"] += lib.ckv_last_launches()
-        return res
+        collect()
+        pending["p"] = p
 
     lib = cache.lib
     for i in range(W):
         one_step(i)
     torch.cuda.synchronize()
+    collect()
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local) if rank == 0 else None
@@ -299,6 +310,7 @@ def main():
         one_step(W + i, ev_a[i])
     t_end.record()
     torch.cuda.synchronize()
+    collect()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / K
@@ -325,12 +337,18 @@ def main():
         if world > 1:
             dist.barrier()
         e0 = time.perf_counter()
+        prev = None
         for i in range(K):
-            res = dec.step(qh[i].to(dev, non_blocking=True))
-            exchange(res)
+            p = dec.step_async(qh[i].to(dev, non_blocking=True), reduce_flags)
+            exchange()
             oh.copy_(dec.out, non_blocking=True)
-            cache.append(kh[i].to(dev, non_blocking=True), vh[i].to(dev, non_blocking=True))
+            cache.append(kh[i].to(dev, non_blocking=True), vh[i].to(dev, non_blocking=True),
+                         validate="defer")
+            if prev is not None:
+                prev.result()  # host reads step i-1's bound report while step i runs
+            prev = p
         torch.cuda.synchronize()
+        prev.result()
         e_ms = (time.perf_counter() - e0) * 1000.0 / K
         if world > 1:
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)

@@ -155,6 +155,10 @@ typedef struct {
   int32_t ecap;             /* exploration samples per head (capacity) */
   int32_t* explore_n;       /* [n_units][n_heads] samples drawn by the host, or NULL */
   int32_t* explore_pos;     /* [n_units][n_heads][ecap] ascending tail positions */
+  const int32_t* unit_group; /* [n_units] Rung-4 group of each unit (e.g. its (layer, sequence)),
+                                or NULL for u / rung4_group */
+  int32_t* group_flags;     /* [n_groups] step-wide Rung-4 request per group */
+  int32_t n_groups;
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136
@@ -207,15 +211,24 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
                            const ckv_scratch* scratch, int32_t host_max_blocks,
                            void* stream);
 
-/* The step in two halves, for callers that must read the decisions before
- * finishing it (the exploration spot check draws its host-side Philox samples
- * from the tail size K' reported by the first half):
- *   ckv_decode_begin: pass A, selection, LRU scratch + page-in (when scratch),
- *                     pass B, combine (certificates written)
- *   ckv_decode_end:   exploration (when st->explore_n), step-wide rung 4,
- *                     dense fallback. */
+/* The step in parts, for callers that must act between them:
+ *   ckv_decode_begin:  pass A, selection, LRU scratch + page-in (when scratch),
+ *                      pass B, combine (certificates written).  The exploration
+ *                      spot check draws its host-side Philox samples from the
+ *                      tail size K' reported here.
+ *   ckv_decode_flags:  exploration (when st->explore_n), then the step-wide
+ *                      Rung-4 request of every group into st->group_flags.
+ *                      A KV-head sharded caller all-reduces (MAX) group_flags
+ *                      across ranks here (harness.py:362-372 per layer).
+ *   ckv_decode_finish: every head of a flagged group returns dense
+ *                      (dense_all_heads); exact dense fallback of rung-3/4 heads.
+ *   ckv_decode_end = ckv_decode_flags + ckv_decode_finish. */
 ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                             const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
+ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                            int32_t host_max_blocks, void* stream);
+ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, int32_t host_max_blocks,
+                             void* stream);
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                           int32_t host_max_blocks, void* stream);
 

@@ -10,7 +10,7 @@ __version__ = "0.1.0"
 from . import _lib, kernels
 from .cache import (DeviceKVCache, ScratchCache, StorageReport, TieredCache, storage_report,
                     storage_table)
-from .engine import (CertifiedDecoder, HeadStepResult, StepOutput, dense_attention,
+from .engine import (CertifiedDecoder, HeadStepResult, PendingStep, StepOutput, dense_attention,
                      run_decode_step)
 from .errors import EmptyCacheError, PagingError, Tier2UnavailableError
 from .harness import (RunResult, Workload, WorkloadConfig, aggregate_telemetry, dump_line,

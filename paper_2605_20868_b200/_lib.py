@@ -62,7 +62,8 @@ class CkvStep(ctypes.Structure):
                 ("work", P), ("n_work", P), ("vlist", P), ("lm2", P), ("head_state", P),
                 ("chunk_state", P), ("page_stats", P), ("prof_begin", P), ("prof_end", P),
                 ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P),
-                ("ecap", I32), ("explore_n", P), ("explore_pos", P)]
+                ("ecap", I32), ("explore_n", P), ("explore_pos", P), ("unit_group", P),
+                ("group_flags", P), ("n_groups", I32)]
 
 
 class CkvScratch(ctypes.Structure):
@@ -99,6 +100,9 @@ def load():
                                    ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_decode_end": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
                                  ctypes.POINTER(CkvStep), I32, P]),
+        "ckv_decode_flags": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
+                                   ctypes.POINTER(CkvStep), I32, P]),
+        "ckv_decode_finish": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvStep), I32, P]),
         "ckv_read_tier1": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, P, P, P, P, P, P, P]),
         "ckv_fault_offset": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, ctypes.c_float, P]),
         "ckv_tier2_drop": (I32, [ctypes.POINTER(CkvCache), I32, I32, P]),
@@ -121,7 +125,8 @@ def exported_symbols():
     return ["ckv_version", "ckv_lru_words", "ckv_scratch_init", "ckv_plan", "ckv_append",
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
             "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
-            "ckv_f64_to_f16", "ckv_last_error", "ckv_decode_begin", "ckv_decode_end"]
+            "ckv_f64_to_f16", "ckv_last_error", "ckv_decode_begin", "ckv_decode_end",
+            "ckv_decode_flags", "ckv_decode_finish"]
 
 
 def check(code, what):

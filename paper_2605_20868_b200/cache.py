@@ -129,7 +129,10 @@ class DeviceKVCache:
         Inputs are cast to FP16 (binary16 ingest, cache.py:82-84).  With
         ``validate`` the sticky device status is read back and a non-finite
         entry raises ValueError; the kernel never mutates the cache when any
-        input is non-finite.
+        input is non-finite.  ``validate="defer"`` skips that host sync: the
+        device still rejects the block, and the ValueError is raised by the
+        next decode step's result (which reads the status with the
+        certificates).
         """
         k = torch.as_tensor(keys, device=self.device)
         v = torch.as_tensor(values, device=self.device)
@@ -146,7 +149,8 @@ class DeviceKVCache:
             raise ValueError(f"append of {n} tokens exceeds the cache capacity "
                              f"({self.max_blocks * B} tokens)")
         k16, v16 = self._to_half(k), self._to_half(v)
-        if validate and (k.dtype != torch.float16):
+        defer = validate == "defer"
+        if validate and not defer and (k.dtype != torch.float16):
             # a finite fp32/fp64 value can overflow binary16: the reference
             # rejects non-finite inputs before the cast (cache.py:80-81)
             if not bool(torch.isfinite(k).all()) or not bool(torch.isfinite(v).all()):
@@ -154,7 +158,7 @@ class DeviceKVCache:
         code = self.lib.ckv_append(ctypes.byref(self.c), _ptr(k16), _ptr(v16), n,
                                    _stream(self.device))
         _lib.check(code, "ckv_append")
-        if validate:
+        if validate and not defer:
             st = self.status.cpu()
             if st[_lib.ST_NONFINITE]:
                 self.status[_lib.ST_NONFINITE] = 0

@@ -14,6 +14,7 @@ cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
 cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, const ckv_scratch*, int,
                           cudaStream_t);
 cudaError_t launch_dense(const ckv_cache*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_group_flags(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
@@ -98,7 +99,8 @@ static bool step_ok(const ckv_cache* c, const ckv_policy* pol, const ckv_step* s
                     int32_t host_max_blocks) {
   if (!cache_ok(c) || !pol || !st || !st->q || !st->out || !st->cert || !st->lm1 ||
       !st->split_state || !st->order || !st->work || !st->n_work || !st->vlist || !st->lm2 ||
-      !st->head_state || !st->chunk_state || !st->dense_list || !st->dense_part)
+      !st->head_state || !st->chunk_state || !st->dense_list || !st->dense_part ||
+      !st->group_flags || st->n_groups < 1 || (!st->unit_group && st->rung4_group < 1))
     return false;
   return host_max_blocks >= 0 && host_max_blocks <= c->max_blocks;
 }
@@ -111,8 +113,8 @@ ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step*
   return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, S(stream)));
 }
 
-ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                          int32_t host_max_blocks, void* stream) {
+ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                            int32_t host_max_blocks, void* stream) {
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   cudaError_t e = cudaSuccess;
   if (st->explore_n) {
@@ -120,8 +122,22 @@ ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* s
     e = ckv::launch_explore(c, pol, st, host_max_blocks, S(stream));
     if (e != cudaSuccess) return st_of(e);
   }
-  e = ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream));
-  return st_of(e);
+  return st_of(ckv::launch_group_flags(c, st, S(stream)));
+}
+
+ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, int32_t host_max_blocks,
+                             void* stream) {
+  ckv_policy dummy{};
+  dummy.k_max = 1;
+  if (!step_ok(c, &dummy, st, host_max_blocks)) return CKV_EINVAL;
+  return st_of(ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream)));
+}
+
+ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                          int32_t host_max_blocks, void* stream) {
+  ckv_status r = ckv_decode_flags(c, pol, st, host_max_blocks, stream);
+  if (r != CKV_OK) return r;
+  return ckv_decode_finish(c, st, host_max_blocks, stream);
 }
 
 ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,

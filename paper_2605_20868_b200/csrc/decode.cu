@@ -315,8 +315,8 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
 }
 
 struct SelSmem {
-  unsigned long long sortk[SEL_MAXSORT];
-  unsigned long long cand[SEL_MAXSORT];
+  int hist[2048];                         // radix-select histogram
+  unsigned long long cand[SEL_MAXSORT];   // candidates, then sorted (descending)
   double cum[SEL_MAXSORT];
   float qv[D];
   float ps[B];
@@ -437,13 +437,16 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   const float lsef = (float)lse;
   const double pmass = (pl > 0) ? exp((double)lmp - lse) : 0.0;
 
-  // ---- top K_sel blocks by l' (ties -> lower index): bisection on the key ----------
+  // ---- top K_sel blocks by l' (ties -> lower index) -------------------------------
+  // T = the K_sel-th largest key by a 3-digit (11/11/10 bit) radix select over
+  // shared histograms, then the candidates (all keys > T, the first keys == T
+  // in block order) are sorted descending by (key, -block) with a bitonic sort.
   const int kwant = (pol.rung1_enabled ? 2 * pol.k_max : pol.k_max) + 1;
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
   int n_sorted = 0;
   if (ksel > 0) {
-    // T = the largest key value with count(key >= T) >= ksel; bisection over
-    // [min key, max key] with one barrier per step (double-buffered partials)
+    // digits of (key - min key), 11 bits at a time from the top of the occupied
+    // range, so the first histogram spreads over the keys actually present
     uint32_t kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
@@ -465,27 +468,52 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       kmx = max(kmx, (uint32_t)S.wsum2[w]);
     }
     __syncthreads();
-    uint32_t lo = kmn;                                   // count(key >= kmn) = nb >= ksel
-    unsigned long long hi = (unsigned long long)kmx + 1; // count(key >= kmx+1) = 0 < ksel
-    int par = 0;
-    while (hi - lo > 1ull) {
-      const uint32_t mid = (uint32_t)((lo + hi) >> 1);
-      int cnt = 0;
-#pragma unroll
-      for (int j = 0; j < KPT; ++j) cnt += (kk[j] >= mid);
-      cnt = __reduce_add_sync(0xffffffffu, cnt);
-      int* buf = par ? S.wsum2 : S.wsum;
-      if (lane == 0) buf[warp] = cnt;
+    const int nbits = (kmx > kmn) ? 32 - __clz(kmx - kmn) : 0;
+    uint32_t prefix = 0, pmask = 0;
+    int need = ksel;
+    for (int top = nbits; top > 0;) {
+      const int shift = max(top - 11, 0);
+      const int nbins = 1 << (top - shift);
+      for (int i = tid; i < 2048; i += SEL_THREADS) S.hist[i] = 0;
       __syncthreads();
-      int tot = 0;
 #pragma unroll
-      for (int w = 0; w < SEL_THREADS / 32; ++w) tot += buf[w];
-      par ^= 1;
-      if (tot >= ksel) lo = mid;
-      else hi = mid;
+      for (int j = 0; j < KPT; ++j) {
+        const uint32_t rel = kk[j] - kmn;
+        const bool in = base + j < nb && (rel & pmask) == prefix;
+        const uint32_t bin = (rel >> shift) & (uint32_t)(nbins - 1);
+        // warp-aggregated increment: one atomic per distinct bin per warp
+        const uint32_t grp = __match_any_sync(0xffffffffu, in ? bin : 0xffffffffu);
+        if (in && lane == __ffs(grp) - 1) atomicAdd(&S.hist[bin], __popc(grp));
+      }
+      __syncthreads();
+      // suffix counts from the top bin down: thread t owns bins [hi-per, hi)
+      const int per = (nbins + SEL_THREADS - 1) / SEL_THREADS;
+      const int hi_bin = nbins - tid * per;
+      int loc = 0;
+      for (int i = 1; i <= per; ++i)
+        if (hi_bin - i >= 0) loc += S.hist[hi_bin - i];
+      const int before = block_excl_scan(loc, S.wsum, &S.misc[8]);  // count in higher bins
+      if (before < need && before + loc >= need) {
+        int run = before;
+        for (int i = 1; i <= per; ++i) {
+          const int cnt = S.hist[hi_bin - i];
+          if (run + cnt >= need) {
+            S.misc[0] = hi_bin - i;
+            S.misc[1] = run;
+            break;
+          }
+          run += cnt;
+        }
+      }
+      __syncthreads();
+      const uint32_t dgt = (uint32_t)S.misc[0];
+      need -= S.misc[1];
+      prefix |= dgt << shift;
+      pmask |= (uint32_t)(nbins - 1) << shift;
+      top = shift;
+      __syncthreads();
     }
-    __syncthreads();
-    const uint32_t T = lo;
+    const uint32_t T = kmn + prefix;
     int ngt = 0, neq = 0;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
@@ -495,7 +523,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     const int off_gt = block_excl_scan(ngt, S.wsum, &S.misc[2]);
     const int tot_gt = S.misc[2];
     const int off_eq = block_excl_scan(neq, S.wsum, &S.misc[3]);
-    const int need = ksel - tot_gt;
+    const int needq = ksel - tot_gt;
     int pg = off_gt, pe = off_eq;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
@@ -505,25 +533,37 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       if (kk[j] > T) {
         S.cand[pg++] = comp;
       } else if (kk[j] == T && b < nb) {
-        if (pe < need) S.cand[tot_gt + pe] = comp;
+        if (pe < needq) S.cand[tot_gt + pe] = comp;
         ++pe;
       }
     }
     n_sorted = ksel;
+    int P = 1;
+    while (P < n_sorted) P <<= 1;
+    for (int i = n_sorted + tid; i < P; i += SEL_THREADS) S.cand[i] = 0ull;
     __syncthreads();
-    // rank sort (composite keys are distinct): position = #greater
-    for (int i = tid; i < n_sorted; i += SEL_THREADS) {
-      const unsigned long long x = S.cand[i];
-      int r = 0;
-      for (int j = 0; j < n_sorted; ++j) r += (S.cand[j] > x);
-      S.sortk[r] = x;
+    // bitonic sort, descending (composite keys are distinct)
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        for (int i = tid; i < P; i += SEL_THREADS) {
+          const int ixj = i ^ j2;
+          if (ixj > i) {
+            const unsigned long long x = S.cand[i], y = S.cand[ixj];
+            const bool desc = (i & k2) == 0;
+            if (desc ? (x < y) : (x > y)) {
+              S.cand[i] = y;
+              S.cand[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
     }
-    __syncthreads();
   }
 
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
   for (int i = tid; i < n_sorted; i += SEL_THREADS) {
-    S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
+    S.cum[i] = (double)expf(ukey((uint32_t)(S.cand[i] >> 32)) - lsef);
   }
   __syncthreads();
   if (warp == 0) {  // prefix sum in fp64 along the mass order (one warp, chunked)
@@ -566,7 +606,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   const int kcov = S.misc[4], kstar = S.misc[5], kp = S.misc[6];
   int32_t* order = st.order + hu * st.kcap;
   for (int i = tid; i < kp; i += SEL_THREADS) {
-    const int b = (int)(0xffffffffu - (uint32_t)(S.sortk[i] & 0xffffffffull));
+    const int b = (int)(0xffffffffu - (uint32_t)(S.cand[i] & 0xffffffffull));
     order[i] = b;
     atomicOr(&fmask[b >> 5], 1u << (b & 31));
   }
@@ -664,7 +704,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     hs.e_tail = et;
     hs.partial_mass = pmass;
     float tm = ninf();
-    if (kp < nb && kp < n_sorted) tm = ukey((uint32_t)(S.sortk[kp] >> 32));
+    if (kp < nb && kp < n_sorted) tm = ukey((uint32_t)(S.cand[kp] >> 32));
     hs.tailmax = tm;
     hs.kprime = kp;
     hs.kstar0 = kstar;

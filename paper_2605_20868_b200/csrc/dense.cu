@@ -26,30 +26,39 @@ struct DenseArgs {
 
 __device__ __forceinline__ float dninf() { return __int_as_float(0xff800000); }
 
-__global__ void k_resolve(DenseArgs a) {
-  // one CTA per rung-4 group
+__device__ __forceinline__ int rung4_group_of(const ckv_step& st, int u) {
+  return st.unit_group ? st.unit_group[u] : u / st.rung4_group;
+}
+
+// every head whose certificate requests Rung 4 flags its unit's group
+__global__ void k_group_flags(DenseArgs a) {
   const ckv_step& st = a.st;
-  const int g0 = blockIdx.x * a.group;
-  const int g1 = min(a.c.n_units, g0 + a.group);
   const int nh = st.n_heads;
-  __shared__ int any4;
-  if (threadIdx.x == 0) any4 = 0;
-  __syncthreads();
-  for (int i = g0 * nh + threadIdx.x; i < g1 * nh; i += blockDim.x) {
-    if (st.cert[i].flags & (CKV_F_CANARY | CKV_F_NUMERIC | CKV_F_EXPLORE)) any4 = 1;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.c.n_units * nh) return;
+  if (st.cert[i].flags & (CKV_F_CANARY | CKV_F_NUMERIC | CKV_F_EXPLORE)) {
+    const int g = rung4_group_of(st, i / nh);
+    if (g >= 0 && g < st.n_groups) atomicOr(&st.group_flags[g], 1);
   }
-  __syncthreads();
-  for (int u = g0 + threadIdx.x; u < g1; u += blockDim.x) {
-    int mask = 0;
-    for (int h = 0; h < nh; ++h) {
-      ckv_cert& ct = st.cert[(size_t)u * nh + h];
-      if (any4) ct.returned_kind = 2;
-      if (ct.returned_kind != 0) mask |= 1 << h;
-    }
-    if (mask) {
-      const int slot = atomicAdd(&st.dense_list[0], 1);
-      st.dense_list[1 + slot] = u | (mask << 24);
-    }
+}
+
+// a flagged group returns dense for all its heads; list the units needing a dense pass
+__global__ void k_resolve(DenseArgs a) {
+  const ckv_step& st = a.st;
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= a.c.n_units) return;
+  const int nh = st.n_heads;
+  const int g = rung4_group_of(st, u);
+  const bool any4 = (g >= 0 && g < st.n_groups) && st.group_flags[g] != 0;
+  int mask = 0;
+  for (int h = 0; h < nh; ++h) {
+    ckv_cert& ct = st.cert[(size_t)u * nh + h];
+    if (any4) ct.returned_kind = 2;
+    if (ct.returned_kind != 0) mask |= 1 << h;
+  }
+  if (mask) {
+    const int slot = atomicAdd(&st.dense_list[0], 1);
+    st.dense_list[1 + slot] = u | (mask << 24);
   }
 }
 
@@ -224,8 +233,17 @@ __global__ void __launch_bounds__(128) k_dense_merge(DenseArgs a) {
 
 extern int g_launches;
 
+cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStream_t s) {
+  DenseArgs a{*c, *st, 0, 0, 0};
+  cudaMemsetAsync(st->group_flags, 0, sizeof(int32_t) * st->n_groups, s);
+  const int n = c->n_units * st->n_heads;
+  k_group_flags<<<(n + 255) / 256, 256, 0, s>>>(a);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_tokens, cudaStream_t s) {
-  DenseArgs a{*c, *st, st->rung4_group > 0 ? st->rung4_group : c->n_units, 0, DN_TOK / B};
+  DenseArgs a{*c, *st, 0, 0, DN_TOK / B};
   // full blocks only (the partial block comes from the head state); at most
   // 160 splits so the merge fits its shared buffers
   const int nblk = (host_max_tokens + B - 1) / B;
@@ -234,8 +252,7 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_to
   if (a.n_dsplit < 1) a.n_dsplit = 1;
   if (a.n_dsplit > st->n_dsplit_cap) a.n_dsplit = st->n_dsplit_cap;
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t), s);
-  const int ngroups = (c->n_units + a.group - 1) / a.group;
-  k_resolve<<<ngroups, 256, 0, s>>>(a);
+  k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
   k_dense<<<dim3(a.n_dsplit, c->n_units), DN_WARPS * 32, 0, s>>>(a);
   k_dense_merge<<<c->n_units, 128, 0, s>>>(a);
   g_launches += 3;

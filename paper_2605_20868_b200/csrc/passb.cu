@@ -437,45 +437,77 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   st.out[hu * D + tid] = out;
   __syncthreads();
 
+  // ---- ranking: top-r of the phase-2 log-masses over F (ties -> lower block
+  // index) against the phase-1 order prefix (fallback.py:164-187,
+  // harness.py:231-250); one block-wide argmax per rank, all threads
+  const int kp = hs.kprime;
+  const int r = pol.ranking_depth;
+  const int32_t* order = st.order + hu * st.kcap;
+  const float* lm2 = st.lm2 + hu * c.max_blocks;
+  __shared__ int picked[64];
+  __shared__ float rvw[4];
+  __shared__ int rbw[4];
+  __shared__ int same_s;
+  __shared__ float rth_s;
+  const bool do_rank = pol.ranking_checks_enabled && kp > 0 && kp >= r;
+  if (do_rank) {
+    const int rr = min(r, 64);
+    if (tid == 0) same_s = 1;
+    for (int j = 0; j < rr; ++j) {
+      float bv = ninf();
+      int bb = 0x7fffffff;
+      for (int i = tid; i < kp; i += blockDim.x) {
+        const int bi = order[i];
+        bool used = false;
+        for (int q = 0; q < j; ++q) used |= (picked[q] == bi);
+        if (used) continue;
+        const float v = lm2[bi];
+        if (bb == 0x7fffffff || v > bv || (v == bv && bi < bb)) {
+          bv = v;
+          bb = bi;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int ob = __shfl_xor_sync(0xffffffffu, bb, o);
+        if (ob != 0x7fffffff && (bb == 0x7fffffff || ov > bv || (ov == bv && ob < bb))) {
+          bv = ov;
+          bb = ob;
+        }
+      }
+      if ((tid & 31) == 0) {
+        rvw[tid >> 5] = bv;
+        rbw[tid >> 5] = bb;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        float v0 = rvw[0];
+        int b0 = rbw[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+          if (rbw[w] != 0x7fffffff && (b0 == 0x7fffffff || rvw[w] > v0 || (rvw[w] == v0 && rbw[w] < b0))) {
+            v0 = rvw[w];
+            b0 = rbw[w];
+          }
+        }
+        picked[j] = b0;
+        rth_s = v0;
+        if (order[j] != b0) same_s = 0;
+      }
+      __syncthreads();
+    }
+  }
+
   if (tid == 0) {
     ckv_cert& ct = st.cert[hu];
     uint32_t fl = ct.flags;
-    const int kp = hs.kprime;
-    const int r = pol.ranking_depth;
-    const int32_t* order = st.order + hu * st.kcap;
-    const float* lm2 = st.lm2 + hu * c.max_blocks;
     const double delta = (double)hs.delta;
     if (pol.ranking_checks_enabled && kp > 0) {
       if (kp < r) {
         fl |= CKV_F_RANKING;
       } else {
-        // top-r of the phase-2 log-masses (ties -> lower block index) against
-        // the phase-1 order prefix (fallback.py:164-187, harness.py:231-250)
-        int picked[64];
-        float rth = 0.f;
-        bool same = true;
-        const int rr = min(r, 64);
-        for (int j = 0; j < rr; ++j) {
-          int best = -1, bb = 0x7fffffff;
-          float bv = 0.f;
-          for (int i = 0; i < kp; ++i) {
-            const int bi = order[i];
-            bool used = false;
-            for (int q = 0; q < j; ++q) used |= (picked[q] == bi);
-            if (used) continue;
-            const float v = lm2[bi];
-            if (best < 0 || v > bv || (v == bv && bi < bb)) {
-              best = i;
-              bv = v;
-              bb = bi;
-            }
-          }
-          picked[j] = bb;
-          rth = bv;
-          if (order[j] != bb) same = false;
-        }
-        if (!same) fl |= CKV_F_RANKING;
-        if (hs.tailmax != ninf() && !((double)hs.tailmax + delta <= (double)rth)) fl |= CKV_F_BOUNDARY;
+        if (!same_s) fl |= CKV_F_RANKING;
+        if (hs.tailmax != ninf() && !((double)hs.tailmax + delta <= (double)rth_s)) fl |= CKV_F_BOUNDARY;
       }
     }
     if (pol.canary_enabled && kp > 0) {

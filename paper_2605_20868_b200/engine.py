@@ -54,6 +54,24 @@ class StepOutput:
         return self.decoder.vlist[u, h, :nv].cpu().numpy()
 
 
+class PendingStep:
+    """Handle of a step enqueued by ``CertifiedDecoder.step_async``."""
+
+    def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens):
+        self._args = (cert_h, stat_h, ps_h, n_tokens)
+        self._dec, self._ev, self._res = dec, event, None
+
+    def done(self):
+        return self._ev.query()
+
+    def result(self):
+        """Wait for this step's certificates (not for later steps) and decode them."""
+        if self._res is None:
+            self._ev.synchronize()
+            self._res = self._dec._output(*self._args)
+        return self._res
+
+
 class CertifiedDecoder:
     """Certified decode over every unit of a DeviceKVCache.
 
@@ -103,8 +121,25 @@ class CertifiedDecoder:
                         ("page_stats", self.page_stats), ("dense_list", self.dense_list),
                         ("dense_part", self.dense_part), ("explore_pos", self.explore_pos)):
             setattr(st, name, _ptr(t))
-        self.rung4_group = int(rung4_group or U)
-        st.rung4_group = self.rung4_group
+        # step-wide Rung 4 (harness.py:362-372) acts on groups of units: one
+        # group = the reference's single step (None), contiguous runs of
+        # ``rung4_group`` units (int), or explicit group ids per unit (array,
+        # e.g. the (layer, sequence) of every unit -- shared across ranks)
+        if rung4_group is None or np.isscalar(rung4_group):
+            g = int(rung4_group or U)
+            groups = np.arange(U) // g
+        else:
+            groups = np.asarray(rung4_group, dtype=np.int64).reshape(-1)
+            if groups.shape[0] != U or groups.min() < 0:
+                raise ValueError("rung4_group must give a non-negative group id per unit")
+        self.unit_group_host = groups
+        self.n_groups = int(groups.max()) + 1
+        self.unit_group = torch.as_tensor(groups, dtype=torch.int32).to(dev)
+        self.group_flags = torch.zeros((self.n_groups,), dtype=torch.int32, device=dev)
+        st.rung4_group = 1
+        st.unit_group = _ptr(self.unit_group)
+        st.group_flags = _ptr(self.group_flags)
+        st.n_groups = self.n_groups
         self.st = st
         self.scratch = scratch
         if scratch is not None:
@@ -114,15 +149,25 @@ class CertifiedDecoder:
         self.ps_host = torch.zeros((U, 4), dtype=torch.int32).pin_memory()
 
     # -- the device step -----------------------------------------------------
-    def launch(self, queries=None):
-        """Enqueue the fast path only (no host sync); returns immediately."""
+    def launch(self, queries=None, reduce_flags=None):
+        """Enqueue the whole step (no host sync); returns immediately.
+
+        ``reduce_flags(group_flags)`` -- e.g. an all-reduce(MAX) across the
+        ranks of a KV-head sharded job -- runs between the Rung-4 requests and
+        their resolution, in stream order (ckv_decode_flags / _finish)."""
         if queries is not None:
             self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
         sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
-        code = self.lib.ckv_decode_step(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                        ctypes.byref(self.st), sc, self.cache.num_blocks,
-                                        _stream(self.cache.device))
-        _lib.check(code, "ckv_decode_step")
+        args = (ctypes.byref(self.cache.c), ctypes.byref(self.pol_c), ctypes.byref(self.st))
+        nbk, stream = self.cache.num_blocks, _stream(self.cache.device)
+        if reduce_flags is None:
+            _lib.check(self.lib.ckv_decode_step(*args, sc, nbk, stream), "ckv_decode_step")
+            return
+        _lib.check(self.lib.ckv_decode_begin(*args, sc, nbk, stream), "ckv_decode_begin")
+        _lib.check(self.lib.ckv_decode_flags(*args, nbk, stream), "ckv_decode_flags")
+        reduce_flags(self.group_flags)
+        _lib.check(self.lib.ckv_decode_finish(ctypes.byref(self.cache.c), ctypes.byref(self.st),
+                                              nbk, stream), "ckv_decode_finish")
 
     def step(self, queries, rng=None):
         """Certified attention for all units: queries [U, nh, 128] (float64).
@@ -143,24 +188,61 @@ class CertifiedDecoder:
         self.launch(queries)
         return self._finish()
 
+    def step_async(self, queries, reduce_flags=None):
+        """Enqueue a certified step and return a ``PendingStep`` without a host
+        sync: the certificate array is copied into one of two pinned buffers
+        behind the step's kernels, so the host can read step i's bound report
+        while the device runs step i+1.  The output stays on the device
+        (``self.out``, valid in stream order until the next step overwrites
+        it); dense rungs are already applied there."""
+        if self.cache.num_tokens == 0:
+            raise EmptyCacheError("cannot attend over an empty cache")
+        if self.policy.exploration_rate > 0:
+            raise ValueError("step_async does not run the exploration spot check; use step()")
+        self.launch(queries, reduce_flags)
+        k = self._ring_i = (getattr(self, "_ring_i", 1) + 1) % 2
+        if not hasattr(self, "_ring"):
+            shp = self.cert_host.shape
+            self._ring = [(torch.zeros(shp, dtype=torch.uint8).pin_memory(),
+                           torch.zeros((8,), dtype=torch.int32).pin_memory(),
+                           torch.zeros(self.ps_host.shape, dtype=torch.int32).pin_memory(),
+                           torch.cuda.Event()) for _ in range(2)]
+            self._ring_pending = [None, None]
+        prev = self._ring_pending[k]
+        if prev is not None:
+            prev.result()  # decode the step that last used this buffer before reusing it
+        cert_h, stat_h, ps_h, ev = self._ring[k]
+        cert_h.copy_(self.cert_buf, non_blocking=True)
+        stat_h.copy_(self.cache.status, non_blocking=True)
+        if self.scratch is not None:
+            ps_h.copy_(self.page_stats, non_blocking=True)
+        ev.record(torch.cuda.current_stream(self.cache.device))
+        pend = PendingStep(self, cert_h, stat_h, ps_h, ev, self.cache.num_tokens)
+        self._ring_pending[k] = pend
+        return pend
+
     def _finish(self):
         self.cert_host.copy_(self.cert_buf, non_blocking=True)
         self.status_host.copy_(self.cache.status, non_blocking=True)
         if self.scratch is not None:
             self.ps_host.copy_(self.page_stats, non_blocking=True)
         torch.cuda.current_stream(self.cache.device).synchronize()  # the step's only host sync
-        st = self.status_host
-        if st[_lib.ST_TIER2]:
+        return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens)
+
+    def _output(self, cert_h, stat_h, ps_h, n_tokens):
+        if stat_h[_lib.ST_NONFINITE]:  # a deferred append check (DeviceKVCache.append)
+            self.cache.status[_lib.ST_NONFINITE] = 0
+            raise ValueError("non-finite key/value entry (append rejected on the device)")
+        if stat_h[_lib.ST_TIER2]:
             self.cache.status[_lib.ST_TIER2] = 0
             raise Tier2UnavailableError("full-precision originals of a promoted block are unavailable")
-        cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh).copy()
+        cert = cert_h.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh).copy()
         kinds = cert["returned_kind"].copy()
-        U, g = self.cache.n_units, self.rung4_group
-        staging = 0
-        for g0 in range(0, U, g):
-            if (kinds[g0:g0 + g] == 2).any():
-                staging += min(g, U - g0) * 2 * self.cache.num_tokens * D * 2
-        ps = self.ps_host.numpy().copy() if self.scratch is not None else None
+        # Rung-4 staging bytes (fallback.py:235-238): every unit of a flagged group
+        flagged = np.unique(self.unit_group_host[(kinds == 2).any(axis=1)])
+        n_units = int(np.isin(self.unit_group_host, flagged).sum()) if flagged.size else 0
+        staging = n_units * 2 * n_tokens * D * 2
+        ps = ps_h.numpy().copy() if self.scratch is not None else None
         return StepOutput(self.out, cert, kinds, ps, staging, self)
 
     def _step_explore(self, queries, rng):
