@@ -316,7 +316,8 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
 
 struct SelSmem {
   int hist[2048];                         // radix-select histogram
-  unsigned long long cand[SEL_MAXSORT];   // candidates, then sorted (descending)
+  unsigned long long cand[SEL_MAXSORT];   // candidates (block order)
+  unsigned long long sortk[SEL_MAXSORT];  // candidates sorted descending
   double cum[SEL_MAXSORT];
   float qv[D];
   float ps[B];
@@ -328,7 +329,7 @@ struct SelSmem {
 };
 
 template <int KPT>
-__global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
+__global__ void __launch_bounds__(SEL_THREADS, 2) k_select(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
   uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
@@ -343,6 +344,13 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   const size_t hu = (size_t)u * nh + h;
   const float* lm = st.lm1 + hu * c.max_blocks;
   HeadState& hs = *reinterpret_cast<HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+
+  // ---- this thread's blocks tid + SEL_THREADS * j (j < KPT): order keys of l'_b in
+  // registers; strided ownership keeps every load coalesced
+#define BJ(j) (tid + SEL_THREADS * (j))
+  uint32_t kk[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) kk[j] = (BJ(j) < nb) ? okey(__ldg(lm + BJ(j))) : 0u;
 
   if (tid < D) S.qv[tid] = (float)(st.q[hu * D + tid] * 0.08838834764831845);
   for (int i = tid; i < (c.max_blocks + 31) / 32; i += SEL_THREADS) fmask[i] = 0u;
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     __syncthreads();
     float L = 0.f, O = 0.f;
     if (M != ninf() && tid < D) {
-#pragma unroll 8
+#pragma unroll 16
       for (int s2 = 0; s2 < nsp; ++s2) {
         const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
         const float sc = (float)S.cum[s2];
@@ -409,28 +417,16 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     __syncthreads();
   }
 
-  // ---- this thread's blocks [tid*KPT, tid*KPT+KPT): order keys of l'_b in registers
-  const int base = tid * KPT;
-  uint32_t kk[KPT];
-#pragma unroll
-  for (int j = 0; j < KPT; j += 4) {
-    if (base + j + 3 < nb && ((reinterpret_cast<uintptr_t>(lm + base + j) & 15u) == 0)) {
-      const float4 x = *reinterpret_cast<const float4*>(lm + base + j);
-      kk[j] = okey(x.x); kk[j + 1] = okey(x.y); kk[j + 2] = okey(x.z); kk[j + 3] = okey(x.w);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) kk[j + q] = (base + j + q < nb) ? okey(lm[base + j + q]) : 0u;
-    }
-  }
-
   // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
   float lmax = lmp;
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, (base + j < nb) ? ukey(kk[j]) : ninf());
+  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, (BJ(j) < nb) ? ukey(kk[j]) : ninf());
   lmax = block_max_f(lmax, S.redf);
   float sef = 0.f;
+  const float lmax2 = lmax * 1.4426950408889634f;
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) sef += (base + j < nb) ? expf(ukey(kk[j]) - lmax) : 0.f;
+  for (int j = 0; j < KPT; ++j)
+    sef += (BJ(j) < nb) ? ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lmax2)) : 0.f;
   double se = block_sum_d((double)sef, S.redd);
   if (pl > 0) se += exp((double)lmp - (double)lmax);
   const double lse = (double)lmax + log(se);
@@ -441,8 +437,11 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   // T = the K_sel-th largest key by a 3-digit (11/11/10 bit) radix select over
   // shared histograms, then the candidates (all keys > T, the first keys == T
   // in block order) are sorted descending by (key, -block) with a bitonic sort.
-  const int kwant = (pol.rung1_enabled ? 2 * pol.k_max : pol.k_max) + 1;
+  // the sorted prefix covers every block that can be promoted (K' <= 2 K_max
+  // with rung 1); the largest tail key comes from a reduction below
+  const int kwant = pol.rung1_enabled ? 2 * pol.k_max : pol.k_max;
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
+  const int sort_cap = max(ksel, SEL_THREADS);  // one rank-sort round
   int n_sorted = 0;
   if (ksel > 0) {
     // digits of (key - min key), 11 bits at a time from the top of the occupied
@@ -450,7 +449,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     uint32_t kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
-      if (base + j < nb) {
+      if (BJ(j) < nb) {
         kmn = min(kmn, kk[j]);
         kmx = max(kmx, kk[j]);
       }
@@ -469,9 +468,14 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     }
     __syncthreads();
     const int nbits = (kmx > kmn) ? 32 - __clz(kmx - kmn) : 0;
+    // Radix passes until the keys >= the current bin's lower edge number at
+    // most SEL_MAXSORT (normally one pass): those are the candidates, sorted
+    // below.  Only when a single key value holds too many blocks does the
+    // exact K_sel-th key T and its tie rule (lower block index first) apply.
     uint32_t prefix = 0, pmask = 0;
-    int need = ksel;
-    for (int top = nbits; top > 0;) {
+    int need = ksel, above = 0, n_cand = nb;
+    bool exact = nb > sort_cap;
+    for (int top = nbits; top > 0 && exact;) {
       const int shift = max(top - 11, 0);
       const int nbins = 1 << (top - shift);
       for (int i = tid; i < 2048; i += SEL_THREADS) S.hist[i] = 0;
@@ -479,11 +483,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
         const uint32_t rel = kk[j] - kmn;
-        const bool in = base + j < nb && (rel & pmask) == prefix;
-        const uint32_t bin = (rel >> shift) & (uint32_t)(nbins - 1);
-        // warp-aggregated increment: one atomic per distinct bin per warp
-        const uint32_t grp = __match_any_sync(0xffffffffu, in ? bin : 0xffffffffu);
-        if (in && lane == __ffs(grp) - 1) atomicAdd(&S.hist[bin], __popc(grp));
+        const bool in = BJ(j) < nb && (rel & pmask) == prefix;
+        if (in) atomicAdd(&S.hist[(rel >> shift) & (uint32_t)(nbins - 1)], 1);
       }
       __syncthreads();
       // suffix counts from the top bin down: thread t owns bins [hi-per, hi)
@@ -500,6 +501,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
           if (run + cnt >= need) {
             S.misc[0] = hi_bin - i;
             S.misc[1] = run;
+            S.misc[2] = cnt;
             break;
           }
           run += cnt;
@@ -507,63 +509,82 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       }
       __syncthreads();
       const uint32_t dgt = (uint32_t)S.misc[0];
-      need -= S.misc[1];
+      const int run = S.misc[1], binc = S.misc[2];
+      __syncthreads();
+      above += run;
+      need -= run;
       prefix |= dgt << shift;
       pmask |= (uint32_t)(nbins - 1) << shift;
       top = shift;
-      __syncthreads();
+      if (above + binc <= sort_cap) {
+        exact = false;
+        n_cand = above + binc;
+      }
     }
     const uint32_t T = kmn + prefix;
-    int ngt = 0, neq = 0;
+    if (!exact) {
+      // candidates: every key >= T (the lower edge of the last bin), block order
+      int nc = 0;
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      ngt += (kk[j] > T);
-      neq += (kk[j] == T && base + j < nb);
-    }
-    const int off_gt = block_excl_scan(ngt, S.wsum, &S.misc[2]);
-    const int tot_gt = S.misc[2];
-    const int off_eq = block_excl_scan(neq, S.wsum, &S.misc[3]);
-    const int needq = ksel - tot_gt;
-    int pg = off_gt, pe = off_eq;
+      for (int j = 0; j < KPT; ++j) nc += (BJ(j) < nb && kk[j] >= T);
+      int pc = block_excl_scan(nc, S.wsum, &S.misc[3]);
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const int b = base + j;
-      const unsigned long long comp =
-          ((unsigned long long)kk[j] << 32) | (unsigned long long)(0xffffffffu - (uint32_t)b);
-      if (kk[j] > T) {
-        S.cand[pg++] = comp;
-      } else if (kk[j] == T && b < nb) {
-        if (pe < needq) S.cand[tot_gt + pe] = comp;
-        ++pe;
+      for (int j = 0; j < KPT; ++j) {
+        const int b = BJ(j);
+        if (b < nb && kk[j] >= T)
+          S.cand[pc++] = ((unsigned long long)kk[j] << 32) |
+                         (unsigned long long)(0xffffffffu - (uint32_t)b);
       }
+      n_sorted = n_cand;
+    } else {
+      // T is the K_sel-th largest key itself: all keys > T, then the first == T
+      // in block order; blocks run j-major (BJ), so one scan per j (rare path)
+      int ngt = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) ngt += (kk[j] > T);
+      int pg = block_excl_scan(ngt, S.wsum, &S.misc[2]);
+      const int tot_gt = S.misc[2];
+#pragma unroll
+      for (int j = 0; j < KPT; ++j)
+        if (kk[j] > T)
+          S.cand[pg++] = ((unsigned long long)kk[j] << 32) |
+                         (unsigned long long)(0xffffffffu - (uint32_t)BJ(j));
+      int taken = tot_gt;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        if (taken >= ksel) continue;  // uniform across the block
+        const bool eq = BJ(j) < nb && kk[j] == T;
+        const int pos = taken + block_excl_scan((int)eq, S.wsum, &S.misc[3]);
+        const int cnt = S.misc[3];
+        if (eq && pos < ksel)
+          S.cand[pos] = ((unsigned long long)kk[j] << 32) |
+                        (unsigned long long)(0xffffffffu - (uint32_t)BJ(j));
+        taken += cnt;
+      }
+      n_sorted = ksel;
     }
-    n_sorted = ksel;
-    int P = 1;
-    while (P < n_sorted) P <<= 1;
-    for (int i = n_sorted + tid; i < P; i += SEL_THREADS) S.cand[i] = 0ull;
     __syncthreads();
-    // bitonic sort, descending (composite keys are distinct)
-    for (int k2 = 2; k2 <= P; k2 <<= 1) {
-      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
-        for (int i = tid; i < P; i += SEL_THREADS) {
-          const int ixj = i ^ j2;
-          if (ixj > i) {
-            const unsigned long long x = S.cand[i], y = S.cand[ixj];
-            const bool desc = (i & k2) == 0;
-            if (desc ? (x < y) : (x > y)) {
-              S.cand[i] = y;
-              S.cand[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
+    // rank sort (composite keys are distinct): position = #greater; the
+    // candidate list is read as broadcast 16-byte pairs
+    for (int i = tid; i < n_sorted; i += SEL_THREADS) {
+      const unsigned long long x = S.cand[i];
+      int r = 0;
+      const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(S.cand);
+      int j = 0;
+#pragma unroll 4
+      for (; j + 1 < n_sorted; j += 2) {
+        const ulonglong2 y = c2[j >> 1];
+        r += (y.x > x) + (y.y > x);
       }
+      if (j < n_sorted) r += (S.cand[j] > x);
+      S.sortk[r] = x;
     }
+    __syncthreads();
   }
 
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
   for (int i = tid; i < n_sorted; i += SEL_THREADS) {
-    S.cum[i] = (double)expf(ukey((uint32_t)(S.cand[i] >> 32)) - lsef);
+    S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
   }
   __syncthreads();
   if (warp == 0) {  // prefix sum in fp64 along the mass order (one warp, chunked)
@@ -606,26 +627,31 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
   const int kcov = S.misc[4], kstar = S.misc[5], kp = S.misc[6];
   int32_t* order = st.order + hu * st.kcap;
   for (int i = tid; i < kp; i += SEL_THREADS) {
-    const int b = (int)(0xffffffffu - (uint32_t)(S.cand[i] & 0xffffffffull));
+    const int b = (int)(0xffffffffu - (uint32_t)(S.sortk[i] & 0xffffffffull));
     order[i] = b;
     atomicOr(&fmask[b >> 5], 1u << (b & 31));
   }
   __syncthreads();
 
   // ---- tail mass, rung 2, E_val tail (fallback.py:141-161, certifier.py:153-160) ----
-  const float* eta = c.eta + (size_t)u * c.max_blocks;
   const bool r2 = pol.rung2_enabled != 0;
   const bool greedy = r2 && pol.greedy_value_budget >= 0.0;
   // greedy budget mode: promote in descending p*eta (ties -> lower index) while the
   // residual exceeds the budget; realised as a threshold T on the contribution key
   // (all keys > T, plus the first `take` keys == T in block order)
+  // this thread's eta values, vector-loaded up front (one latency, not KPT)
+  const float* eta = c.eta + (size_t)u * c.max_blocks;
+  float etv[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) etv[j] = (BJ(j) < nb) ? __ldg(eta + BJ(j)) : 0.f;
+  const float lse2 = lsef * 1.4426950408889634f;
   uint32_t gT = 0xffffffffu;
   int take = 0;
   if (greedy && nb > 0) {
     double tot = 0.0;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
-      if (base + j < nb) tot += (double)(expf(ukey(kk[j]) - lsef) * eta[base + j]);
+      if (BJ(j) < nb) tot += (double)(ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) * etv[j]);
     tot = block_sum_d(tot, S.redd);
     const double need = tot - pol.greedy_value_budget;
     if (need > 0.0) {
@@ -636,8 +662,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
         double g = 0.0;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
-          if (base + j >= nb) continue;
-          const float cj = expf(ukey(kk[j]) - lsef) * eta[base + j];
+          if (BJ(j) >= nb) continue;
+          const float cj = ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) * etv[j];
           if (__float_as_uint(cj) >= mid) g += (double)cj;
         }
         g = block_sum_d(g, S.redd);
@@ -649,8 +675,8 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       int neq = 0;
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
-        if (base + j >= nb) continue;
-        const float cj = expf(ukey(kk[j]) - lsef) * eta[base + j];
+        if (BJ(j) >= nb) continue;
+        const float cj = ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) * etv[j];
         if (__float_as_uint(cj) > gT) ggt += (double)cj;
         neq += (__float_as_uint(cj) == gT);
       }
@@ -662,31 +688,43 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
       take = m - eq_before;  // how many of this thread's == T blocks are promoted
     }
   }
-  double at = 0.0, et = 0.0;
+  // masses p_b = exp(l'_b - lse): fp32 via MUFU ex2, per-thread sums in fp32,
+  // across threads in fp64
+  const float vtol = (float)pol.v_tol;
+  float atf = 0.f, etf = 0.f, tmx = ninf();
   int nv = 0;
   uint32_t vb[(KPT + 31) / 32];
 #pragma unroll
   for (int w = 0; w < (KPT + 31) / 32; ++w) vb[w] = 0u;
-#pragma unroll
-  for (int j = 0; j < KPT; ++j) {
-    const int b = base + j;
-    if (b >= nb) continue;
-    const float pf = expf(ukey(kk[j]) - lsef);
-    const double pb = (double)pf;
-    const bool inF = (fmask[b >> 5] >> (b & 31)) & 1u;
-    const double pe = pb * (double)eta[b];
-    bool inV;
-    if (greedy) {
-      const uint32_t ck = __float_as_uint(pf * eta[b]);
-      inV = (gT != 0xffffffffu) && (ck > gT || (ck == gT && take-- > 0));
-    } else {
-      inV = r2 && (pe > pol.v_tol);
-    }
-    if (!inF) at += pb;
-    if (!inF && !inV) et += pe;
+  auto account = [&](int j, bool valid, float pf, float pe, bool inV) {
+    const bool inF = valid && ((fmask[BJ(j) >> 5] >> (BJ(j) & 31)) & 1u);
+    atf += inF ? 0.f : pf;
+    tmx = fmaxf(tmx, (valid && !inF) ? ukey(kk[j]) : ninf());
+    etf += (inF || inV) ? 0.f : pe;
     nv += inV;
     vb[j >> 5] |= (uint32_t)inV << (j & 31);
+  };
+  if (greedy) {
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const bool valid = BJ(j) < nb;
+      const float pf = valid ? ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) : 0.f;
+      const float pe = pf * etv[j];
+      const uint32_t ck = __float_as_uint(pe);
+      const bool inV = valid && (gT != 0xffffffffu) && (ck > gT || (ck == gT && take-- > 0));
+      account(j, valid, pf, pe, inV);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const bool valid = BJ(j) < nb;
+      const float pf = valid ? ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) : 0.f;
+      const float pe = pf * etv[j];
+      account(j, valid, pf, pe, r2 && valid && (pe > vtol));
+    }
   }
+  double at = (double)atf, et = (double)etf;
+  tmx = block_max_f(tmx, S.redf);  // largest phase-1 log-mass over the tail
   at = block_sum_d(at, S.redd);
   et = block_sum_d(et, S.redd);
   const int vo = block_excl_scan(nv, S.wsum, &S.misc[7]);
@@ -696,16 +734,14 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(StepArgs a) {
     int pv = vo;
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
-      if ((vb[j >> 5] >> (j & 31)) & 1u) vlist[pv++] = base + j;
+      if ((vb[j >> 5] >> (j & 31)) & 1u) vlist[pv++] = BJ(j);
   }
   if (tid == 0) {
     hs.lse = lse;
     hs.alpha_hat = (kp >= nb) ? 0.0 : at;
     hs.e_tail = et;
     hs.partial_mass = pmass;
-    float tm = ninf();
-    if (kp < nb && kp < n_sorted) tm = ukey((uint32_t)(S.cand[kp] >> 32));
-    hs.tailmax = tm;
+    hs.tailmax = (kp < nb) ? tmx : ninf();
     hs.kprime = kp;
     hs.kstar0 = kstar;
     hs.n_v = n_v;
