@@ -183,33 +183,56 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   const PageView& pv = a.pv;
   const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
   const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
-  auto key_src = [&](int b2) -> const uint16_t* {  // scratch slot if resident, else Tier-2
-    const int sl = kslot ? kslot[b2] : -1;
-    return (sl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + sl) * B * D : c.tier2_k + (ubk + b2) * B * D;
+  // Per-item metadata is software-pipelined so no dependent global load sits
+  // on the critical path: work entries are read two items ahead, the slot /
+  // key-scale / eta / Tier-2-valid words of an item one iteration before its
+  // TMA is issued (the item after that) and consumed.
+  struct Meta {
+    int e, sl, valid;
+    float smax, eta;
   };
-  auto issue = [&](int item, int stg) {
-    const int e2 = work[item];
+  auto load_meta = [&](int e2, bool ok) -> Meta {  // work entries may have bit 31 set
+    Meta m;
+    m.e = e2;
     const int b2 = e2 & 0xffffff;
-    const bool keys = ((uint32_t)e2 >> 24) & 0xfu;
+    m.sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
+    m.smax = ok ? c.kscale_max[ubk + b2] : 1.f;
+    m.eta = ok ? eta[b2] : 0.f;
+    m.valid = ok ? c.tier2_valid[ubk + b2] : 1;
+    return m;
+  };
+  auto issue = [&](const Meta& m, int stg) {
+    const int b2 = m.e & 0xffffff;
+    const bool keys = ((uint32_t)m.e >> 24) & 0xfu;
     mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
     bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
-    if (keys) bulk_g2s(S.kt[warp][stg], key_src(b2), B * D * 2, &S.bar[warp][stg]);
+    if (keys) {
+      const uint16_t* src = (m.sl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
+                                        : c.tier2_k + (ubk + b2) * B * D;
+      bulk_g2s(S.kt[warp][stg], src, B * D * 2, &S.bar[warp][stg]);
+    }
   };
   int cur = item_at(0);
-  if (lane == 0 && cur >= 0) issue(cur, 0);
+  int i1 = item_at(1);
+  Meta mc = load_meta(cur >= 0 ? work[cur] : 0, cur >= 0);
+  Meta mn = load_meta(i1 >= 0 ? work[i1] : 0, i1 >= 0);
+  if (lane == 0 && cur >= 0) issue(mc, 0);
   for (int k = 0; cur >= 0; ++k) {
     const int stg = k & 1;
-    const int nxt = item_at(k + 1);
+    const int nxt = i1;
+    const int i2 = item_at(k + 2);
+    const int e_nn = (i2 >= 0) ? work[i2] : 0;  // consumed at the end of this iteration
     if (lane == 0 && nxt >= 0) {
       fence_proxy_async();
-      issue(nxt, stg ^ 1);
+      issue(mn, stg ^ 1);
     }
-    const int e = work[cur];
+    const int e = mc.e;
     const int b = e & 0xffffff;
     const uint32_t fm = ((uint32_t)e >> 24) & 0xfu, vm = ((uint32_t)e >> 28) & 0xfu;
     const bool inF = (fm >> h) & 1u, inV = (vm >> h) & 1u;
-    if ((fm | vm) && lane == 0 && !c.tier2_valid[ubk + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
-    const float smax = c.kscale_max[ubk + b];
+    if ((fm | vm) && lane == 0 && !mc.valid) atomicOr(&c.status[CKV_ST_TIER2], 1);
+    const float smax = mc.smax;
+    const float eta_b = mc.eta;
     mbar_wait(&S.bar[warp][stg], (uint32_t)(k >> 1) & 1u);
     const uint8_t* rec = S.rec[warp][stg];
 
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
           lm2[b] = lb;
           const double rb = exp((double)lb - lse);
           sF += rb;
-          if (!inV) eF += rb * (double)eta[b];
+          if (!inV) eF += rb * (double)eta_b;
         }
       }
     }
@@ -314,6 +337,9 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
     }
     __syncwarp();
     cur = nxt;
+    i1 = i2;
+    mc = mn;
+    mn = load_meta(e_nn, i2 >= 0);
   }
 
   // ---- reduce within the warp (per head), then across the 4 warps ----------
