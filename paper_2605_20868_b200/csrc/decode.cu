@@ -18,6 +18,7 @@
 // Every additive decomposition is over blocks, so the result equals the
 // reference's single mask-gated pass (attention.py:227-300) up to fp32
 // rounding.
+#include <cstdlib>
 #include "step.cuh"
 
 namespace ckv {
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int u = blockIdx.y, sp = blockIdx.x;
+  const int u = a.u0 + blockIdx.y, sp = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
   const int nb = c.n_blocks[u];
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_select(StepArgs a) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const ckv_policy& pol = a.pol;
-  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+  const int h = blockIdx.x, u = a.u0 + blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int nh = st.n_heads;
   const int nb = c.n_blocks[u];
@@ -808,44 +809,33 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // launchers
 // =============================================================================
 extern int g_launches;
-cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&,
+cudaError_t launch_union(const ckv_cache*, const ckv_policy*, const ckv_step*, int, int, cudaStream_t);
+cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&, int, int,
                          cudaStream_t);
-cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
+cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, int, cudaStream_t);
 
-cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                          const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
-  g_launches = 0;
-  StepArgs a{*c, *st, *pol, PageView{}};
-  const size_t smA = sizeof(PassASmem);
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
-    cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attrs = true;
-  }
-  const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
-  if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
-  if (nsplit_used > 0) {
-    k_pass_a<<<dim3(nsplit_used, c->n_units), PA_WARPS * 32, smA, s>>>(a);
-    ++g_launches;
-  }
-  if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
+// Everything after pass A for units [u0, u0 + nu): selection, the union work
+// list, LRU scratch (+ page-in), pass B, combine.
+static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                               const ckv_scratch* sc, int host_max_blocks, int u0, int nu,
+                               cudaStream_t s) {
+  StepArgs a{*c, *st, *pol, PageView{}, u0};
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
   if (nbh <= SEL_THREADS * 32)
-    k_select<32><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+    k_select<32><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 64)
-    k_select<64><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+    k_select<64><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else
-    k_select<128><<<dim3(st->n_heads, c->n_units), SEL_THREADS, smS, s>>>(a);
+    k_select<128><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  e = launch_union(c, pol, st, u0, nu, s);
+  if (e != cudaSuccess) return e;
   PageView pv{};
   if (sc) {
-    e = launch_scratch(c, st, sc, s);  // LRU accounting (+ side-stream page-in into slots)
+    e = launch_scratch(c, st, sc, u0, nu, s);  // LRU accounting (+ side-stream page-in into slots)
     if (e != cudaSuccess) return e;
     pv.kslots = sc->key_slots;
     pv.vslots = sc->value_slots;
@@ -856,7 +846,82 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
     pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
     pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
   }
-  return launch_passb(c, pol, st, pv, s);
+  return launch_passb(c, pol, st, pv, u0, nu, s);
+}
+
+static cudaStream_t tail_stream() {  // high priority: tail kernels jump ahead of pass-A CTAs
+  static cudaStream_t s = nullptr;
+  if (!s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi);
+  }
+  return s;
+}
+
+// Optional unit chunks (CKV_CHUNKS=n): pass A of chunk k+1 runs while the
+// tail of chunk k runs on a second, high-priority stream.  Units are
+// independent, so the result is identical to one launch over all units.  Off
+// by default: pass A fills every SM's register file (4 x 128 threads x 126
+// registers), so tail CTAs displace pass-A CTAs instead of filling gaps
+// (measured at C3: 1 chunk 2.47 ms, 2 chunks 2.53, 4 chunks 2.69).
+static int decode_chunks(int n_units) {
+  const char* env = getenv("CKV_CHUNKS");
+  int n = env ? atoi(env) : 1;
+  if (n_units < 16) n = 1;
+  return max(1, min(n, n_units));
+}
+
+cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                          const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
+  g_launches = 0;
+  const size_t smA = sizeof(PassASmem);
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+    cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attrs = true;
+  }
+  const int U = c->n_units;
+  const int nch = decode_chunks(U);
+  const int per = (U + nch - 1) / nch;
+  const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
+  cudaStream_t s2 = (nch > 1) ? tail_stream() : s;
+  cudaError_t e = cudaSuccess;
+  if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
+  cudaEvent_t evs[64];
+  int nev = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int u0 = k * per, nu = min(per, U - u0);
+    if (nu <= 0) break;
+    StepArgs a{*c, *st, *pol, PageView{}, u0};
+    if (nsplit_used > 0) {
+      k_pass_a<<<dim3(nsplit_used, nu), PA_WARPS * 32, smA, s>>>(a);
+      ++g_launches;
+    }
+    if (k == nch - 1 || u0 + nu >= U) {
+      if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);
+    }
+    if (nch > 1) {
+      cudaEventCreateWithFlags(&evs[nev], cudaEventDisableTiming);
+      cudaEventRecord(evs[nev], s);
+      cudaStreamWaitEvent(s2, evs[nev], 0);
+      ++nev;
+    }
+    e = launch_tail(c, pol, st, sc, host_max_blocks, u0, nu, s2);
+    if (e != cudaSuccess) break;
+  }
+  if (nch > 1) {
+    cudaEventCreateWithFlags(&evs[nev], cudaEventDisableTiming);
+    cudaEventRecord(evs[nev], s2);
+    cudaStreamWaitEvent(s, evs[nev], 0);
+    ++nev;
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_block_logmass(const double* sc, const int64_t* bnd, int nb, double* bm,

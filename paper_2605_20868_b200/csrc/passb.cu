@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(UN_THREADS) k_union(StepArgs a) {
   extern __shared__ __align__(16) uint32_t ub[];
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int u = blockIdx.x, tid = threadIdx.x;
+  const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
   const int nh = st.n_heads;
   const int nb = c.n_blocks[u];
   const int W = (c.max_blocks + 31) / 32;
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int ck = blockIdx.x, u = blockIdx.y;
+  const int ck = blockIdx.x, u = a.u0 + blockIdx.y;
   const int C = gridDim.x;
   const int IPC = st.items_per_chunk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const ckv_policy& pol = a.pol;
-  const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
+  const int h = blockIdx.x, u = a.u0 + blockIdx.y, tid = threadIdx.x;
   const int nh = st.n_heads;
   const size_t hu = (size_t)u * nh + h;
   const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
@@ -561,20 +561,32 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
 
 extern int g_launches;
 
-cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                         const PageView& pv, cudaStream_t s) {
-  StepArgs a{*c, *st, *pol, pv};
+static void passb_attrs() {
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
     cudaFuncSetAttribute(k_union, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
+}
+
+cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st, int u0, int nu,
+                         cudaStream_t s) {
+  passb_attrs();
+  StepArgs a{*c, *st, *pol, PageView{}, u0};
   const int W = (c->max_blocks + 31) / 32;
-  k_union<<<c->n_units, UN_THREADS, 2 * H * W * 4, s>>>(a);
-  k_pass_b<<<dim3(st->n_chunks, c->n_units), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
-  k_combine<<<dim3(st->n_heads, c->n_units), 128, 0, s>>>(a);
-  g_launches += 3;
+  k_union<<<nu, UN_THREADS, 2 * H * W * 4, s>>>(a);
+  g_launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
+                         const PageView& pv, int u0, int nu, cudaStream_t s) {
+  passb_attrs();
+  StepArgs a{*c, *st, *pol, pv, u0};
+  k_pass_b<<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  k_combine<<<dim3(st->n_heads, nu), 128, 0, s>>>(a);
+  g_launches += 2;
   return cudaGetLastError();
 }
 

@@ -62,13 +62,14 @@ struct LruArgs {
   int32_t* miss_list;  // [U][2][miss_cap]
   int32_t* miss_n;     // [U][2]
   int32_t miss_cap;
+  int32_t u0;
 };
 
 __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   extern __shared__ __align__(16) int32_t sm[];
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int u = blockIdx.x, tid = threadIdx.x;
+  const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
   const int maxb = c.max_blocks;
   const int nb = c.n_blocks[u];
   int32_t* L = a.state + (size_t)u * a.words;
@@ -249,9 +250,92 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   }
 }
 
+// Scratch that holds every block (capacity >= max_blocks, ring size 0): no
+// eviction can happen, so ScratchCache.request reduces to "the first request of
+// a block that is not resident is a miss, every other request a hit" -- per
+// block of the step's union work list (k_union: ascending, with the mask of
+// requesting heads), one thread per item; misses get the next free slots in
+// block order.  Same counters, page stats, stamps and miss list as k_lru.
+__global__ void __launch_bounds__(LRU_THREADS) k_lru_fast(LruArgs ka, LruArgs va) {
+  const int kind = blockIdx.y;
+  const LruArgs& a = kind ? va : ka;
+  const ckv_step& st = a.st;
+  const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
+  const int maxb = a.c.max_blocks;
+  int32_t* L = a.state + (size_t)u * a.words;
+  int32_t* stamp = L + 4;
+  int32_t* slot = L + 4 + maxb;  // R == 0
+  const int nwork = st.n_work[u];
+  const int32_t* work = st.work + (size_t)u * st.wcap;
+  __shared__ int ws[32];
+  __shared__ int misc[4];
+  const int T0 = L[0], count0 = L[2];
+  int32_t* mlist = a.miss_list ? a.miss_list + ((size_t)u * 2 + kind) * a.miss_cap : nullptr;
+  long long hits = 0, misses = 0;
+  int base_m = 0, base_req = 0;
+  for (int i0 = 0; i0 < nwork; i0 += LRU_THREADS) {
+    const int i = i0 + tid;
+    int nreq = 0, miss = 0, b = 0;
+    if (i < nwork) {
+      const uint32_t e = (uint32_t)work[i];
+      b = (int)(e & 0xffffffu);
+      nreq = __popc((e >> (kind ? 28 : 24)) & 0xfu);
+      if (nreq) miss = (stamp[b] == 0);
+    }
+    const int rank = blk_scan_excl(miss, ws, &misc[0]);
+    const int nm = misc[0];
+    const int roff = blk_scan_excl(nreq, ws, &misc[1]);
+    const int nr = misc[1];
+    if (nreq) {
+      if (a.cap > 0) {
+        if (miss) {
+          slot[b] = count0 + base_m + rank;
+          if (mlist && base_m + rank < a.miss_cap) mlist[base_m + rank] = b;
+        }
+        stamp[b] = T0 + base_req + roff + nreq - 1;  // stamp of its last request
+      }
+      misses += (a.cap > 0) ? miss : nreq;
+      hits += (a.cap > 0) ? nreq - miss : 0;
+    }
+    base_m += nm;
+    base_req += nr;
+  }
+  // block totals
+  __shared__ long long red[2][LRU_THREADS / 32];
+  long long hsum = hits, msum = misses;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+    msum += __shfl_xor_sync(0xffffffffu, msum, o);
+  }
+  if ((tid & 31) == 0) {
+    red[0][tid >> 5] = hsum;
+    red[1][tid >> 5] = msum;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    long long H2 = 0, M2 = 0;
+    for (int w = 0; w < LRU_THREADS / 32; ++w) {
+      H2 += red[0][w];
+      M2 += red[1][w];
+    }
+    if (a.cap > 0) {
+      L[0] = T0 + base_req;
+      L[2] = count0 + base_m;
+    }
+    st.page_stats[u * 4 + 2 * kind + 0] = (int32_t)H2;
+    st.page_stats[u * 4 + 2 * kind + 1] = (int32_t)M2;
+    int64_t* ctr = a.counters + (size_t)u * 6 + 3 * kind;
+    ctr[0] += H2;
+    ctr[1] += M2;
+    ctr[2] += M2 * (long long)(B * D * 2);
+    if (a.miss_n) a.miss_n[u * 2 + kind] = (a.cap > 0) ? min(base_m, a.miss_cap) : 0;
+  }
+}
+
 // gather: Tier-2 (pinned host, zero-copy) -> HBM slots for this step's misses
-__global__ void __launch_bounds__(256) k_pagein(ckv_cache c, ckv_scratch sc, int32_t kw, int32_t vw) {
-  const int u = blockIdx.x, kind = blockIdx.y, tid = threadIdx.x;
+__global__ void __launch_bounds__(256) k_pagein(ckv_cache c, ckv_scratch sc, int32_t kw, int32_t vw, int32_t u0) {
+  const int u = u0 + blockIdx.x, kind = blockIdx.y, tid = threadIdx.x;
   const int maxb = c.max_blocks;
   const int cap = kind ? sc.value_capacity : sc.key_capacity;
   uint16_t* slots = kind ? sc.value_slots : sc.key_slots;
@@ -294,20 +378,31 @@ static cudaStream_t side_stream() {
   return s;
 }
 
-cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc,
+cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc, int u0, int nu,
                            cudaStream_t s) {
   int words[2];
+  LruArgs la[2];
+  bool fast = true;
   for (int kind = 0; kind < 2; ++kind) {
     const int cap = kind ? sc->value_capacity : sc->key_capacity;
     const int R = lru_ring(c->max_blocks, cap);
     words[kind] = 4 + 2 * c->max_blocks + R;
-    LruArgs a{*c, *st, kind ? sc->value_lru : sc->key_lru, words[kind], cap, kind, sc->counters,
-              sc->miss_list, sc->miss_n, sc->miss_cap};
-    const size_t smem = (size_t)(c->max_blocks + R + c->max_blocks + c->max_blocks + 1024 +
-                                 c->max_blocks + (c->max_blocks + 31) / 32 + 4) * 4;
-    cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_lru<<<c->n_units, LRU_THREADS, smem, s>>>(a);
+    la[kind] = LruArgs{*c, *st, kind ? sc->value_lru : sc->key_lru, words[kind], cap, kind, sc->counters,
+                       sc->miss_list, sc->miss_n, sc->miss_cap, u0};
+    fast = fast && (R == 0);
+  }
+  if (fast) {  // no eviction possible for either kind: one light pass over the union list
+    k_lru_fast<<<dim3(nu, 2), LRU_THREADS, 0, s>>>(la[0], la[1]);
     ++g_launches;
+  } else {
+    for (int kind = 0; kind < 2; ++kind) {
+      const int R = lru_ring(c->max_blocks, la[kind].cap);
+      const size_t smem = (size_t)(c->max_blocks + R + c->max_blocks + c->max_blocks + 1024 +
+                                   c->max_blocks + (c->max_blocks + 31) / 32 + 4) * 4;
+      cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_lru<<<nu, LRU_THREADS, smem, s>>>(la[kind]);
+      ++g_launches;
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -319,7 +414,7 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
     cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
     cudaEventRecord(fork, s);
     cudaStreamWaitEvent(side, fork, 0);
-    k_pagein<<<dim3(c->n_units, 2), 256, 0, side>>>(*c, *sc, words[0], words[1]);
+    k_pagein<<<dim3(nu, 2), 256, 0, side>>>(*c, *sc, words[0], words[1], u0);
     ++g_launches;
     cudaEventRecord(join, side);
     cudaStreamWaitEvent(s, join, 0);

@@ -40,6 +40,7 @@ struct StepArgs {
   ckv_step st;
   ckv_policy pol;
   PageView pv;
+  int32_t u0;  // first unit of this launch (units u0 + blockIdx)
 };
 
 // Exponent S of the unit's value scaling: every fp16 product p' * scale with
