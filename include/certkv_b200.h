@@ -150,7 +150,8 @@ typedef struct {
   void* prof_end;
   int32_t rung4_group;      /* units sharing a step-wide rung 4 (0 = all units) */
   int32_t n_dsplit_cap;     /* dense-fallback splits per unit (from ckv_plan) */
-  int32_t* dense_list;      /* [1 + n_units] count, then unit | head_mask << 24 */
+  int32_t* dense_list;      /* [1 + 2 n_units] count, per-item split counters, then
+                               unit | head_mask << 24 per dense item */
   float* dense_part;        /* [n_units][n_dsplit_cap][4][132] dense split states */
   int32_t ecap;             /* exploration samples per head (capacity) */
   int32_t* explore_n;       /* [n_units][n_heads] samples drawn by the host, or NULL */
@@ -159,6 +160,9 @@ typedef struct {
                                 or NULL for u / rung4_group */
   int32_t* group_flags;     /* [n_groups] step-wide Rung-4 request per group */
   int32_t n_groups;
+  int32_t* unit_done;       /* [n_units] zero-initialised, self-resetting: the last q-head
+                               selection of a unit builds its union work list (NULL: a
+                               separate launch does) */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136

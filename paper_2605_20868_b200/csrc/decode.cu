@@ -759,6 +759,20 @@ __global__ void __launch_bounds__(SEL_THREADS, 2) k_select(StepArgs a) {
     if (kcov != kstar) fl |= CKV_F_CLAMPED;
     ct.flags = fl;
   }
+  // the last q-head of the unit to finish builds the unit's union work list
+  if (st.unit_done) {
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int prev = atomicAdd(&st.unit_done[u], 1);
+      last = (prev == nh - 1);
+      if (last) st.unit_done[u] = 0;
+      __threadfence();
+    }
+    __syncthreads();
+    if (last) build_union(c, st, u, reinterpret_cast<uint32_t*>(&S), S.wsum);
+  }
 }
 
 // =============================================================================
@@ -831,8 +845,10 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  e = launch_union(c, pol, st, u0, nu, s);
-  if (e != cudaSuccess) return e;
+  if (!st->unit_done) {  // otherwise built by the last selection CTA of each unit
+    e = launch_union(c, pol, st, u0, nu, s);
+    if (e != cudaSuccess) return e;
+  }
   PageView pv{};
   if (sc) {
     e = launch_scratch(c, st, sc, u0, nu, s);  // LRU accounting (+ side-stream page-in into slots)

@@ -7,8 +7,8 @@
 //   k_dense        exact softmax attention over the FP16 originals (full
 //                  blocks from Tier-2 + the partial block), fp32, split over
 //                  the sequence; the four q-heads of a unit share each K/V read.
-//   k_dense_merge  merges the splits and overwrites the fast-path output of
-//                  every dense head.
+//                  The last split CTA of a unit to finish merges the splits and
+//                  overwrites the fast-path output of every dense head.
 #include "step.cuh"
 
 namespace ckv {
@@ -58,8 +58,80 @@ __global__ void k_resolve(DenseArgs a) {
   }
   if (mask) {
     const int slot = atomicAdd(&st.dense_list[0], 1);
-    st.dense_list[1 + slot] = u | (mask << 24);
+    st.dense_list[1 + a.c.n_units + slot] = u | (mask << 24);
   }
+}
+
+// Merge the splits of one dense item and overwrite the output of its dense
+// heads (run by the last split CTA of the item to finish).
+__device__ void dense_merge_item(const DenseArgs& a, int item) {
+  const ckv_cache& c = a.c;
+  const ckv_step& st = a.st;
+  const int e = st.dense_list[1 + c.n_units + item];
+  const int u = e & 0xffffff, mask = (e >> 24) & 0xf;
+  const int nh = st.n_heads;
+  const int tid = threadIdx.x;
+  const int pl = c.partial_len[u];
+  const int ns = a.n_dsplit;
+  __shared__ float sm_m[H][160], sm_sc[H][160];
+  __shared__ float red[H][4];
+  const float* p0 = st.dense_part + ((size_t)item * ns * H) * 132;
+  // per-split maxima -> per-head frame, splits spread over the threads
+  for (int i = tid; i < ns * H; i += blockDim.x) sm_m[i % H][i / H] = __ldcg(p0 + (size_t)i * 132);
+  __syncthreads();
+  if (tid < H * 32) {
+    const int h = tid >> 5, l = tid & 31;
+    float m = dninf();
+    for (int s = l; s < ns; s += 32) m = fmaxf(m, sm_m[h][s]);
+    m = warp_max(m);
+    if (l == 0) red[h][0] = m;
+  }
+  __syncthreads();
+  for (int i = tid; i < ns * H; i += blockDim.x) {
+    const int h = i % H, s = i / H;
+    const HeadState& hs =
+        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + (h < nh ? h : 0)) * CKV_HEAD_FLOATS);
+    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
+    sm_sc[h][s] = (sm_m[h][s] == dninf()) ? 0.f : expf(sm_m[h][s] - M);
+  }
+  __syncthreads();
+  for (int h = 0; h < nh; ++h) {
+    if (!((mask >> h) & 1)) continue;
+    const HeadState& hs =
+        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + h) * CKV_HEAD_FLOATS);
+    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
+    float L = 0.f, O = 0.f;
+#pragma unroll 8
+    for (int s = 0; s < ns; ++s) {
+      const float* p = p0 + (s * H + h) * 132;
+      const float sc = sm_sc[h][s];
+      L += __ldcg(p + 1) * sc;
+      O += __ldcg(p + 4 + tid) * sc;
+    }
+    if (pl > 0) {
+      const float sc = expf(hs.mp - M);
+      L += hs.lp * sc;
+      O += hs.np_[tid] * sc;
+    }
+    st.out[((size_t)u * nh + h) * D + tid] = O / L;
+  }
+}
+
+// Called by every split CTA of a dense item once its state is written: the
+// last one merges (device-scope counter, reset for the next step).
+__device__ __forceinline__ void dense_split_done(const DenseArgs& a, int item) {
+  __shared__ int last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    int* done = a.st.dense_list + 1 + item;
+    const int prev = atomicAdd(done, 1);
+    last = (prev == a.n_dsplit - 1);
+    if (last) *done = 0;
+    __threadfence();
+  }
+  __syncthreads();
+  if (last) dense_merge_item(a, item);
 }
 
 struct DenseSmem {
@@ -72,16 +144,16 @@ struct DenseSmem {
 // x hi/lo-split q' on the tensor cores, fp32 accumulate); P.V runs on the
 // tensor cores too: A = the fragment-ordered FP16 values (exact), B = the
 // weights as an fp16 hi/lo pair (column 2h + part), fp32 accumulation.  The
-// partial block is added in k_dense_merge from the state k_select computed.
+// partial block is added in the merge from the state k_select computed.
 __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
-  __shared__ DenseSmem S;
-  __shared__ float ow[DN_WARPS][H][D];
+  __shared__ __align__(16) DenseSmem S;
+  __shared__ __align__(16) float ow[DN_WARPS][H][D];
   __shared__ float mw[DN_WARPS][H][2];
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int item = blockIdx.y, sp = blockIdx.x;
   if (item >= st.dense_list[0]) return;
-  const int e = st.dense_list[1 + item];
+  const int e = st.dense_list[1 + c.n_units + item];
   const int u = e & 0xffffff;
   const int nh = st.n_heads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -90,6 +162,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
   float* outp = st.dense_part + (((size_t)item * a.n_dsplit + sp) * H) * 132;
   if (b0 >= b1) {
     for (int i = tid; i < H * 132; i += blockDim.x) outp[i] = (i % 132 == 0) ? dninf() : 0.f;
+    dense_split_done(a, item);
     return;
   }
   for (int i = tid; i < H * D; i += blockDim.x) {
@@ -175,60 +248,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
     }
     outp[hh * 132 + 4 + tid] = O;
   }
-}
-
-__global__ void __launch_bounds__(128) k_dense_merge(DenseArgs a) {
-  const ckv_cache& c = a.c;
-  const ckv_step& st = a.st;
-  const int item = blockIdx.x;
-  if (item >= st.dense_list[0]) return;
-  const int e = st.dense_list[1 + item];
-  const int u = e & 0xffffff, mask = (e >> 24) & 0xf;
-  const int nh = st.n_heads;
-  const int tid = threadIdx.x;
-  const int pl = c.partial_len[u];
-  const int ns = a.n_dsplit;
-  __shared__ float sm_m[H][160], sm_sc[H][160];
-  __shared__ float red[H][4];
-  const float* p0 = st.dense_part + ((size_t)item * ns * H) * 132;
-  // per-split maxima -> per-head frame, splits spread over the threads
-  for (int i = tid; i < ns * H; i += blockDim.x) sm_m[i % H][i / H] = p0[(size_t)i * 132];
-  __syncthreads();
-  if (tid < H * 32) {
-    const int h = tid >> 5, l = tid & 31;
-    float m = dninf();
-    for (int s = l; s < ns; s += 32) m = fmaxf(m, sm_m[h][s]);
-    m = warp_max(m);
-    if (l == 0) red[h][0] = m;
-  }
-  __syncthreads();
-  for (int i = tid; i < ns * H; i += blockDim.x) {
-    const int h = i % H, s = i / H;
-    const HeadState& hs =
-        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + (h < nh ? h : 0)) * CKV_HEAD_FLOATS);
-    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
-    sm_sc[h][s] = (sm_m[h][s] == dninf()) ? 0.f : expf(sm_m[h][s] - M);
-  }
-  __syncthreads();
-  for (int h = 0; h < nh; ++h) {
-    if (!((mask >> h) & 1)) continue;
-    const HeadState& hs =
-        *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + h) * CKV_HEAD_FLOATS);
-    const float M = (pl > 0) ? fmaxf(red[h][0], hs.mp) : red[h][0];
-    float L = 0.f, O = 0.f;
-    for (int s = 0; s < ns; ++s) {
-      const float* p = p0 + (s * H + h) * 132;
-      const float sc = sm_sc[h][s];
-      L += p[1] * sc;
-      O += p[4 + tid] * sc;
-    }
-    if (pl > 0) {
-      const float sc = expf(hs.mp - M);
-      L += hs.lp * sc;
-      O += hs.np_[tid] * sc;
-    }
-    st.out[((size_t)u * nh + h) * D + tid] = O / L;
-  }
+  dense_split_done(a, item);
 }
 
 extern int g_launches;
@@ -251,11 +271,10 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_to
   a.n_dsplit = (nblk + a.blk_per_split - 1) / a.blk_per_split;
   if (a.n_dsplit < 1) a.n_dsplit = 1;
   if (a.n_dsplit > st->n_dsplit_cap) a.n_dsplit = st->n_dsplit_cap;
-  cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t), s);
+  cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t) * (1 + c->n_units), s);  // count + done counters
   k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
   k_dense<<<dim3(a.n_dsplit, c->n_units), DN_WARPS * 32, 0, s>>>(a);
-  k_dense_merge<<<c->n_units, 128, 0, s>>>(a);
-  g_launches += 3;
+  g_launches += 2;
   return cudaGetLastError();
 }
 

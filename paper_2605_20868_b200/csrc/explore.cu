@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(128) k_explore(StepArgs a) {
   const int W = (nb + 31) / 32;
   uint32_t* fb = sh;               // [W] promoted bitmap
   uint32_t* pre = sh + W;          // [W] tail blocks before word w
-  __shared__ float qh[H * D];
+  __shared__ __align__(16) float qh[H * D];
   __shared__ int fail;
   for (int i = tid; i < W; i += blockDim.x) fb[i] = 0u;
   for (int i = tid; i < H * D; i += blockDim.x) {

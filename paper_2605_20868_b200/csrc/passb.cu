@@ -18,72 +18,12 @@
 
 namespace ckv {
 
-constexpr int UN_THREADS = 512;
+constexpr int UN_THREADS = 256;
 
 __global__ void __launch_bounds__(UN_THREADS) k_union(StepArgs a) {
   extern __shared__ __align__(16) uint32_t ub[];
-  const ckv_cache& c = a.c;
-  const ckv_step& st = a.st;
-  const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
-  const int nh = st.n_heads;
-  const int nb = c.n_blocks[u];
-  const int W = (c.max_blocks + 31) / 32;
-  uint32_t* fb = ub;           // [H][W]
-  uint32_t* vb = ub + H * W;   // [H][W]
   __shared__ int ws[32];
-  __shared__ int tot;
-  for (int i = tid; i < 2 * H * W; i += UN_THREADS) ub[i] = 0u;
-  __syncthreads();
-  for (int h = 0; h < nh; ++h) {
-    const size_t hu = (size_t)u * nh + h;
-    const int kp = st.cert[hu].k_star;
-    const int nv = st.cert[hu].n_value_promoted;
-    const int32_t* ord = st.order + hu * st.kcap;
-    const int32_t* vl = st.vlist + hu * c.max_blocks;
-    for (int i = tid; i < kp; i += UN_THREADS) atomicOr(&fb[h * W + (ord[i] >> 5)], 1u << (ord[i] & 31));
-    for (int i = tid; i < nv; i += UN_THREADS) atomicOr(&vb[h * W + (vl[i] >> 5)], 1u << (vl[i] & 31));
-  }
-  __syncthreads();
-  const int per = (nb + UN_THREADS - 1) / UN_THREADS;
-  const int lo = tid * per, hi = min(nb, lo + per);
-  int cnt = 0;
-  for (int b = lo; b < hi; ++b) {
-    uint32_t any = 0;
-    for (int h = 0; h < nh; ++h) any |= (fb[h * W + (b >> 5)] | vb[h * W + (b >> 5)]) >> (b & 31);
-    cnt += any & 1u;
-  }
-  // block exclusive scan
-  const int lane = tid & 31, warp = tid >> 5;
-  int x = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) ws[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = (lane < UN_THREADS / 32) ? ws[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < UN_THREADS / 32) ws[lane] = w;
-    if (lane == UN_THREADS / 32 - 1) tot = w;
-  }
-  __syncthreads();
-  int pos = ((warp > 0) ? ws[warp - 1] : 0) + x - cnt;
-  int32_t* work = st.work + (size_t)u * st.wcap;
-  for (int b = lo; b < hi; ++b) {
-    uint32_t fm = 0, vm = 0;
-    for (int h = 0; h < nh; ++h) {
-      fm |= ((fb[h * W + (b >> 5)] >> (b & 31)) & 1u) << h;
-      vm |= ((vb[h * W + (b >> 5)] >> (b & 31)) & 1u) << h;
-    }
-    if (fm | vm) work[pos++] = b | (int)(fm << 24) | (int)(vm << 28);
-  }
-  if (tid == 0) st.n_work[u] = tot;
+  build_union(a.c, a.st, a.u0 + blockIdx.x, ub, ws);
 }
 
 // -----------------------------------------------------------------------------

@@ -62,4 +62,75 @@ __device__ __forceinline__ float ukey(uint32_t k) {  // inverse of okey
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
+// The union work list of unit u: every block some q-head promotes (F_h) or
+// value-promotes (V_h), ascending, as block | F-mask << 24 | V-mask << 28.
+// Word-parallel over the per-head bitmaps; ub = 2 * H * ceil(nb / 32) words of
+// shared memory, ws = 32 ints; blockDim.x a multiple of 32.
+__device__ inline void build_union(const ckv_cache& c, const ckv_step& st, int u, uint32_t* ub,
+                                   int* ws) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int nh = st.n_heads;
+  const int nb = c.n_blocks[u];
+  const int W = (nb + 31) / 32;
+  uint32_t* fb = ub;           // [H][W]
+  uint32_t* vb = ub + H * W;   // [H][W]
+  for (int i = tid; i < 2 * H * W; i += nt) ub[i] = 0u;
+  __syncthreads();
+  for (int h = 0; h < nh; ++h) {
+    const size_t hu = (size_t)u * nh + h;
+    const int kp = __ldcg(&st.cert[hu].k_star);
+    const int nv = __ldcg(&st.cert[hu].n_value_promoted);
+    const int32_t* ord = st.order + hu * st.kcap;
+    const int32_t* vl = st.vlist + hu * c.max_blocks;
+    for (int i = tid; i < kp; i += nt) {
+      const int b = __ldcg(ord + i);
+      atomicOr(&fb[h * W + (b >> 5)], 1u << (b & 31));
+    }
+    for (int i = tid; i < nv; i += nt) {
+      const int b = __ldcg(vl + i);
+      atomicOr(&vb[h * W + (b >> 5)], 1u << (b & 31));
+    }
+  }
+  __syncthreads();
+  int32_t* work = st.work + (size_t)u * st.wcap;
+  int base = 0;
+  for (int w0 = 0; w0 < W; w0 += nt) {
+    const int w = w0 + tid;
+    uint32_t any = 0;
+    if (w < W)
+      for (int h = 0; h < nh; ++h) any |= fb[h * W + w] | vb[h * W + w];
+    const int cnt = __popc(any);
+    int x = cnt;  // block-wide exclusive scan of the per-word counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < nw; ++k) {
+      const int v = ws[k];
+      before += (k < warp) ? v : 0;
+      total += v;
+    }
+    int pos = base + before + x - cnt;
+    while (any) {
+      const int bit = __ffs(any) - 1;
+      any &= any - 1;
+      const int b = w * 32 + bit;
+      uint32_t fm = 0, vm = 0;
+      for (int h = 0; h < nh; ++h) {
+        fm |= ((fb[h * W + w] >> bit) & 1u) << h;
+        vm |= ((vb[h * W + w] >> bit) & 1u) << h;
+      }
+      work[pos++] = b | (int)(fm << 24) | (int)(vm << 28);
+    }
+    base += total;
+    __syncthreads();
+  }
+  if (tid == 0) st.n_work[u] = base;
+}
+
 }  // namespace ckv

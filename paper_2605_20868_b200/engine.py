@@ -106,7 +106,8 @@ class CertifiedDecoder:
         self.chunk_state = torch.zeros((U, st.n_chunks, 4, _lib.CHUNK_FLOATS),
                                        dtype=torch.float32, device=dev)
         self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
-        self.dense_list = torch.zeros((U + 1,), dtype=torch.int32, device=dev)
+        self.dense_list = torch.zeros((2 * U + 1,), dtype=torch.int32, device=dev)
+        self.unit_done = torch.zeros((U,), dtype=torch.int32, device=dev)
         st.ecap = max(1, int(round(0.05 * NB)) + 1)
         self.explore_n = torch.zeros((U, nh), dtype=torch.int32, device=dev)
         self.explore_pos = torch.zeros((U, nh, st.ecap), dtype=torch.int32, device=dev)
@@ -119,7 +120,8 @@ class CertifiedDecoder:
                         ("vlist", self.vlist), ("lm2", self.lm2),
                         ("head_state", self.head_state), ("chunk_state", self.chunk_state),
                         ("page_stats", self.page_stats), ("dense_list", self.dense_list),
-                        ("dense_part", self.dense_part), ("explore_pos", self.explore_pos)):
+                        ("dense_part", self.dense_part), ("explore_pos", self.explore_pos),
+                        ("unit_done", self.unit_done)):
             setattr(st, name, _ptr(t))
         # step-wide Rung 4 (harness.py:362-372) acts on groups of units: one
         # group = the reference's single step (None), contiguous runs of
