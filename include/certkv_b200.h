@@ -163,6 +163,8 @@ typedef struct {
   int32_t* unit_done;       /* [n_units] zero-initialised, self-resetting: the last q-head
                                selection of a unit builds its union work list (NULL: a
                                separate launch does) */
+  int32_t* queue;           /* [2] zero-initialised, self-resetting work-queue counters of the
+                               persistent pass B (NULL: one CTA per (chunk, unit)) */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136

@@ -63,7 +63,8 @@ class CkvStep(ctypes.Structure):
                 ("chunk_state", P), ("page_stats", P), ("prof_begin", P), ("prof_end", P),
                 ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P),
                 ("ecap", I32), ("explore_n", P), ("explore_pos", P), ("unit_group", P),
-                ("group_flags", P), ("n_groups", I32), ("unit_done", P)]
+                ("group_flags", P), ("n_groups", I32), ("unit_done", P),
+                ("queue", P)]
 
 
 class CkvScratch(ctypes.Structure):

@@ -51,13 +51,13 @@ __device__ __forceinline__ void vcode_a(uint32_t w, uint32_t& a0, uint32_t& a1, 
   a3 = h2_fma((w8 & 0x00f000f0u) | magic, k16, m64);
 }
 
-__global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
+// One chunk (IPC consecutive items of unit u's union list, 4 warps interleaved).
+// kb = items this warp has pushed through its 2-stage ring so far (stage and
+// mbarrier parity continue across the chunks a persistent CTA processes).
+__device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, const int u,
+                                             const int ck, const int C, int& kb) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int ck = blockIdx.x, u = a.u0 + blockIdx.y;
-  const int C = gridDim.x;
   const int IPC = st.items_per_chunk;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
@@ -67,17 +67,11 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
     if (tid < H) cs[tid * CKV_CHUNK_FLOATS] = ninf();
     return;
   }
+  __syncthreads();  // the previous chunk's reduction is done with S
   for (int i = tid; i < H * D; i += blockDim.x) {
     const int hh = i / D;
     S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
                         : 0.f;
-  }
-  if (tid == 0) {
-    for (int w = 0; w < PB_WARPS; ++w) {
-      mbar_init(&S.bar[w][0], 1);
-      mbar_init(&S.bar[w][1], 1);
-    }
-    fence_mbar_init();
   }
   __syncthreads();
   QFrag f;
@@ -156,9 +150,13 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   int i1 = item_at(1);
   Meta mc = load_meta(cur >= 0 ? work[cur] : 0, cur >= 0);
   Meta mn = load_meta(i1 >= 0 ? work[i1] : 0, i1 >= 0);
-  if (lane == 0 && cur >= 0) issue(mc, 0);
-  for (int k = 0; cur >= 0; ++k) {
-    const int stg = k & 1;
+  if (lane == 0 && cur >= 0) {
+    fence_proxy_async();
+    issue(mc, kb & 1);
+  }
+  int k = 0;
+  for (; cur >= 0; ++k) {
+    const int stg = (kb + k) & 1;
     const int nxt = i1;
     const int i2 = item_at(k + 2);
     const int e_nn = (i2 >= 0) ? work[i2] : 0;  // consumed at the end of this iteration
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
     if ((fm | vm) && lane == 0 && !mc.valid) atomicOr(&c.status[CKV_ST_TIER2], 1);
     const float smax = mc.smax;
     const float eta_b = mc.eta;
-    mbar_wait(&S.bar[warp][stg], (uint32_t)(k >> 1) & 1u);
+    mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
     const uint8_t* rec = S.rec[warp][stg];
 
     const BlockScores r = phase1_block(f, rec, smax, lane);
@@ -281,6 +279,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
     mc = mn;
     mn = load_meta(e_nn, i2 >= 0);
   }
+  kb += k;
 
   // ---- reduce within the warp (per head), then across the 4 warps ----------
   dden += __shfl_xor_sync(0xffffffffu, dden, 4);
@@ -332,6 +331,47 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
       o[3] = 0.f;
       reinterpret_cast<double*>(o + 4)[0] = E2;
       reinterpret_cast<double*>(o + 4)[1] = S2;
+    }
+  }
+}
+
+// Persistent over (unit, chunk) items pulled from a device queue (balanced
+// tail); without st.queue one CTA per (chunk, unit).
+__global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
+  const ckv_step& st = a.st;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int w = 0; w < PB_WARPS; ++w) {
+      mbar_init(&S.bar[w][0], 1);
+      mbar_init(&S.bar[w][1], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int C = st.n_chunks;
+  int kb = 0;
+  if (!st.queue) {
+    pass_b_chunk(a, S, a.u0 + blockIdx.y, blockIdx.x, C, kb);
+    return;
+  }
+  __shared__ int s_item;
+  const int total = a.nu * C;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(&st.queue[0], 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    pass_b_chunk(a, S, a.u0 + item / C, item % C, C, kb);
+  }
+  if (tid == 0) {  // the last CTA out resets the queue for the next launch
+    __threadfence();
+    if (atomicAdd(&st.queue[1], 1) == (int)gridDim.x - 1) {
+      st.queue[0] = 0;
+      st.queue[1] = 0;
+      __threadfence();
     }
   }
 }
@@ -523,8 +563,21 @@ cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_st
 cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                          const PageView& pv, int u0, int nu, cudaStream_t s) {
   passb_attrs();
-  StepArgs a{*c, *st, *pol, pv, u0};
-  k_pass_b<<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  StepArgs a{*c, *st, *pol, pv, u0, nu};
+  if (st->queue) {
+    static int slots = 0;
+    if (!slots) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pass_b, PB_WARPS * 32, sizeof(PassBSmem));
+      slots = max(1, sms * max(1, per));
+    }
+    const int grid = min(slots, nu * st->n_chunks);
+    k_pass_b<<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  } else {
+    k_pass_b<<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+  }
   k_combine<<<dim3(st->n_heads, nu), 128, 0, s>>>(a);
   g_launches += 2;
   return cudaGetLastError();

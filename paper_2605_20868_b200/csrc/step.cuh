@@ -41,6 +41,7 @@ struct StepArgs {
   ckv_policy pol;
   PageView pv;
   int32_t u0;  // first unit of this launch (units u0 + blockIdx)
+  int32_t nu;  // units in this launch (persistent kernels)
 };
 
 // Exponent S of the unit's value scaling: every fp16 product p' * scale with

@@ -108,6 +108,8 @@ class CertifiedDecoder:
         self.page_stats = torch.zeros((U, 4), dtype=torch.int32, device=dev)
         self.dense_list = torch.zeros((2 * U + 1,), dtype=torch.int32, device=dev)
         self.unit_done = torch.zeros((U,), dtype=torch.int32, device=dev)
+        # st.queue (persistent pass B) stays NULL: measured 443 us vs 416 us for one
+        # CTA per (chunk, unit) at C3 -- the per-chunk ring drain is not overlapped
         st.ecap = max(1, int(round(0.05 * NB)) + 1)
         self.explore_n = torch.zeros((U, nh), dtype=torch.int32, device=dev)
         self.explore_pos = torch.zeros((U, nh, st.ecap), dtype=torch.int32, device=dev)

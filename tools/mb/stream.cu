@@ -37,10 +37,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_stream(const uint8_t* base, int 
   if (acc == 12345.f) sink[0] = acc;
 }
 template <int WARPS, int STAGES>
-void run(const uint8_t* d, size_t nrec, float* sink) {
+void run(const uint8_t* d, size_t nrec, float* sink, size_t pad = 0) {
   const int per = 256;
   const int grid = (int)(nrec / per);
-  const size_t smem = WARPS * STAGES * REC + WARPS * STAGES * 8;
+  const size_t smem = WARPS * STAGES * REC + WARPS * STAGES * 8 + pad;
   cudaFuncSetAttribute(k_stream<WARPS, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
@@ -63,12 +63,10 @@ int main() {
   const size_t nrec = 2097152;  // 9.66 GB as in C3
   uint8_t* d; float* sink;
   cudaMalloc(&d, nrec * REC); cudaMemset(d, 1, nrec * REC); cudaMalloc(&sink, 4);
-  run<4, 2>(d, nrec, sink);
-  run<4, 3>(d, nrec, sink);
-  run<4, 4>(d, nrec, sink);
-  run<8, 2>(d, nrec, sink);
-  run<8, 3>(d, nrec, sink);
-  run<2, 4>(d, nrec, sink);
-  run<16, 2>(d, nrec, sink);
+  run<4, 2>(d, nrec, sink, 56 * 1024 - 4 * 2 * REC);  // 4 CTAs/SM: 32 records in flight / SM
+  run<4, 2>(d, nrec, sink, 75 * 1024 - 4 * 2 * REC);  // 3 CTAs/SM: 24
+  run<4, 2>(d, nrec, sink, 110 * 1024 - 4 * 2 * REC);  // 2 CTAs/SM: 16
+  run<4, 3>(d, nrec, sink, 56 * 1024 - 4 * 3 * REC);  // 4 CTAs/SM: 48
+  run<4, 3>(d, nrec, sink, 75 * 1024 - 4 * 3 * REC);  // 3 CTAs/SM: 36
   return 0;
 }
