@@ -359,3 +359,62 @@ def test_exploration_and_greedy_parity(ck, name, tmp_path):
     path = ck.write_telemetry(dev, str(tmp_path / "run.jsonl"))
     lines = open(path).read().splitlines()
     assert len(lines) == cfg.steps + 2 and '"kernel_backend":"b200"' in lines[0]
+
+
+# ---- adversarial inputs (BASELINE config C5 in miniature) ----------------------------
+
+def test_adversarial_outliers_near_tie_fault(ck):
+    """Outlier key channels (x1000 on two channels), near-tie twin blocks and a
+    corrupted key offset (verification.py:420-428): the batched decoder agrees
+    with the oracle on decisions, kinds and outputs, the fault makes its unit's
+    Rung-4 group dense while the other group stays certified."""
+    wl = make_workload(kind="near_tie", n_tokens=1500, head_dim=128, query_heads=8, kv_heads=2,
+                       steps=3, seed=13, ingest_binary16=True, narrow=True, build_caches=False)
+    keys = wl["keys"].copy()
+    keys[:, :, 3] *= 1000.0
+    keys[:, :, 77] *= 1000.0
+    keys = keys.astype(np.float16).astype(np.float64)
+    vals = wl["values"].astype(np.float16).astype(np.float64)
+    n = 1500
+    kvs = []
+    for u in range(2):
+        kv = oracle.OracleKV(16, 128, 16, ingest_binary16=True, narrow=True)
+        kv.append_tokens(keys[u, :n], vals[u, :n])
+        kvs.append(kv)
+    cache = ck.DeviceKVCache(2, n + 16)
+    cache.append(torch.from_numpy(keys[:, :n]), torch.from_numpy(vals[:, :n]))
+    pol = ck.PolicyConfig(exploration_rate=0.0, k_max=8)
+    opol = OraclePolicy(exploration_rate=0.0, k_max=8)
+    # two Rung-4 groups: unit 0 and unit 1 (as two layers would be)
+    dec = ck.CertifiedDecoder(cache, pol, n_heads=4, rung4_group=[0, 1])
+    for s in range(3):
+        if s == 2:  # corrupt one stored key offset of a block head 0 promotes (both sides)
+            q0 = wl["queries"][s, 0]
+            bf = int(oracle.decode_step(q0, kvs[0], opol)["promoted"][0])
+            ch = int(np.argmax(np.abs(q0)))
+            # raise the block's phase-1 scores so it stays promoted and is checked
+            shift = float(np.sign(q0[ch]) * 50.0 * (1.0 + np.abs(kvs[0].kscale[bf]).sum()))
+            cache.corrupt_offset(0, bf, ch, shift)
+            kvs[0].corrupt_offset(bf, ch, shift)
+        q = torch.from_numpy(wl["queries"][s].reshape(2, 4, 128)).cuda()
+        res = dec.step(q)
+        out = res.out.double().cpu().numpy()
+        refs = [oracle.decode_step(wl["queries"][s, h], kvs[h // 4], opol) for h in range(8)]
+        for u in range(2):
+            any4 = any(refs[4 * u + j]["flags"][3] for j in range(4))
+            for j in range(4):
+                r = refs[4 * u + j]
+                row = res.cert[u, j]
+                ctx = (s, u, j)
+                assert int(row["k_star"]) == r["k_star"], ctx
+                want = "dense_all_heads" if any4 else r["kind"]
+                assert ck.engine.KINDS[int(res.kinds[u, j])] == want, ctx
+                if want == "dense_all_heads" and r["kind"] != "dense_all_heads":
+                    ref_out = oracle.dense_output(wl["queries"][s, 4 * u + j], kvs[u])
+                else:
+                    ref_out = r["output"]
+                err = np.abs(out[u, j] - ref_out).max() / np.abs(ref_out).max()
+                assert err < 1e-4, (ctx, err)
+        if s == 2:
+            assert (res.kinds[0] == 2).all()      # the corrupted unit's group is dense
+            assert not (res.kinds[1] == 2).any()  # the other group is not
