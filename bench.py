@@ -30,23 +30,49 @@ UNIT = "steps/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
+# BASELINE.json configs C2-C5 (C1 is the reference's CPU case: the parity tests
+# and the cpu_baseline leg).  The default bench line is C3, the headline.
+PRESETS = {
+    "c2": dict(ctx=32768, batch=1, tier2="device", scratch=-1, v_tol=None, adversarial=False,
+               desc="C2: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, 32768 ctx, batch 1"),
+    "c3": dict(ctx=131072, batch=1, tier2="device", scratch=-1, v_tol=None, adversarial=False,
+               desc="C3: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, 131072 ctx, batch 1, "
+                    "KV-head sharded"),
+    "c4": dict(ctx=16384, batch=32, tier2="host", scratch=-1, v_tol=1e-3, adversarial=False,
+               desc="C4: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, 16384 ctx, batch 32, "
+                    "tight v_tol (value promotions), Tier-2 in pinned host RAM (page-in)"),
+    "c5": dict(ctx=65536, batch=1, tier2="device", scratch=-1, v_tol=None, adversarial=True,
+               desc="C5: 65536 ctx, outlier key channels (x1000 on 2 channels), near-tie twin "
+                    "blocks, corrupted key offsets in layer 0 (canary -> Rung 4 -> dense)"),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--config", default="c3", choices=sorted(PRESETS))
+    ap.add_argument("--ctx", type=int, default=None)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--kv-heads", type=int, default=8)
     ap.add_argument("--q-per-kv", type=int, default=4)
-    ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--tier2", default="device", choices=["device", "host"])
-    ap.add_argument("--scratch", type=int, default=-1,
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--tier2", default=None, choices=["device", "host"])
+    ap.add_argument("--scratch", type=int, default=None,
                     help="LRU scratch capacity in blocks (-1: every block, 0: off)")
+    ap.add_argument("--v-tol", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    pre = PRESETS[args.config]
+    for k in ("ctx", "batch", "tier2", "scratch", "v_tol"):
+        if getattr(args, k) is None:
+            setattr(args, k, pre[k])
+    args.adversarial = pre["adversarial"]
+    args.desc = pre["desc"]
+    return args
 
 
 def peak_hbm():
@@ -171,13 +197,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     K, W = args.steps, max(3, args.warmup)
     total_units = args.layers * args.kv_heads * args.batch
-    config = {"workload": "C3: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, "
-                          f"{args.ctx} ctx, batch {args.batch}, KV-head sharded",
+    pol_desc = "PolicyConfig(exploration_rate=0.0) defaults"
+    if args.v_tol is not None:
+        pol_desc = f"PolicyConfig(exploration_rate=0.0, v_tol={args.v_tol})"
+    tier1_gb = total_units * args.ctx * 288 / 1e9
+    config = {"workload": args.desc if args.ctx == PRESETS[args.config]["ctx"] else
+              f"{args.config.upper()} shape at {args.ctx} ctx, batch {args.batch}",
               "ctx": args.ctx, "layers": args.layers, "kv_heads": args.kv_heads,
               "q_heads": args.kv_heads * args.q_per_kv, "batch": args.batch,
               "parallelism": f"kv-head shard x{args.gpus}",
-              "policy": "PolicyConfig(exploration_rate=0.0) defaults",
-              "l2": "inputs larger than L2 (Tier-1 9.66 GB/step at 128K)",
+              "policy": pol_desc,
+              "l2": f"inputs larger than L2 (Tier-1 {tier1_gb:.2f} GB/step)",
               "tier2": args.tier2}
 
     if args.impl == "reference":
@@ -220,17 +250,31 @@ def main():
     max_tokens = args.ctx + 2 * (K + W) + 32
     cache = ck.DeviceKVCache(U, max_tokens, device=dev, tier2=args.tier2)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
-    chunk = 4096
+    chunk = max(16, min(4096, (1 << 22) // U))
     t0 = time.perf_counter()
     for pos in range(0, args.ctx, chunk):
         n = min(chunk, args.ctx - pos)
-        kk = torch.randn((U, n, 128), generator=g, device=dev).half()
+        kk = torch.randn((U, n, 128), generator=g, device=dev)
         vv = torch.randn((U, n, 128), generator=g, device=dev).half()
-        cache.append(kk, vv, validate=False)
+        if args.adversarial:
+            kk[:, :, 3] *= 1000.0    # outlier key channels
+            kk[:, :, 77] *= 1000.0
+            if pos == 0 and n >= 32:  # near-tie twin blocks 0 and 1
+                kk[:, 16:32] = kk[:, 0:16] + 1e-4 * torch.randn_like(kk[:, 0:16])
+        cache.append(kk.half(), vv, validate=False)
     torch.cuda.synchronize()
     prefill_s = time.perf_counter() - t0
+    if args.adversarial and rank == 0:
+        # corrupt stored key offsets of 8 blocks of unit 0 (layer 0), random channel and
+        # sign, so some promoted block's scores move by far more than Delta every step
+        # (verification.py:420-428): the canary trips and layer 0 returns dense
+        rs = np.random.default_rng(5)
+        for b in rs.choice(cache.num_blocks, size=8, replace=False):
+            cache.corrupt_offset(0, int(b), int(rs.integers(0, 128)),
+                                 float(rs.choice([-1.0, 1.0]) * 5.0e4))
 
-    pol = ck.PolicyConfig(exploration_rate=0.0)
+    pol = ck.PolicyConfig(exploration_rate=0.0) if args.v_tol is None else \
+        ck.PolicyConfig(exploration_rate=0.0, v_tol=args.v_tol)
     cap = cache.max_blocks if args.scratch < 0 else args.scratch
     scratch = ck.ScratchCache(cap) if args.scratch != 0 else None
     from paper_2605_20868_b200 import sharding
@@ -261,6 +305,7 @@ def main():
 
     launches = {"n": 0}
     dense_heads = {"n": 0}
+    stats = {"rung4": 0, "nv": 0.0, "pagein": 0, "steps": 0}
     last = {}
     pending = {"p": None}
 
@@ -269,6 +314,11 @@ def main():
         if p is not None:
             res = p.result()
             dense_heads["n"] += int((res.kinds != 0).sum())
+            stats["rung4"] += int((res.kinds == 2).sum())
+            stats["nv"] += float(res.cert["n_value_promoted"].mean())
+            if res.page_stats is not None:
+                stats["pagein"] += int(res.page_stats[:, 1].sum() + res.page_stats[:, 3].sum()) * 4096
+            stats["steps"] += 1
             last["res"] = res
             pending["p"] = None
 
@@ -300,6 +350,7 @@ def main():
         time.sleep(0.3)
     launches["n"] = 0
     dense_heads["n"] = 0
+    stats.update(rung4=0, nv=0.0, pagein=0, steps=0)
     nb_timed = cache.num_blocks
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -401,6 +452,9 @@ def main():
         "k_star_mean": float(last["res"].cert["k_star"].mean()),
         "promoted_union_blocks_per_unit": float(dec.n_work.float().mean().item()),
         "dense_heads_in_timed_region": n_dense,
+        "rung4_heads_in_timed_region": stats["rung4"],
+        "value_promoted_per_head_mean": stats["nv"] / max(1, stats["steps"]),
+        "pagein_bytes_per_step": stats["pagein"] / max(1, stats["steps"]),
         "clocks": clocks,
         "prefill_s": prefill_s,
     }

@@ -345,14 +345,28 @@ __global__ void __launch_bounds__(256) k_pagein(ckv_cache c, ckv_scratch sc, int
   const int n = sc.miss_n[u * 2 + kind];
   const int32_t* ml = sc.miss_list + ((size_t)u * 2 + kind) * sc.miss_cap;
   const uint16_t* src0 = kind ? c.tier2_v : c.tier2_k;
-  for (int k = 0; k < n; ++k) {
-    const int b = ml[k];
-    const int s = slot_of[b];
-    if (s < 0) continue;  // evicted again later in the same step: pass B reads Tier-2
-    if (tid == 0 && !c.tier2_valid[(size_t)u * maxb + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
-    const uint4* src = reinterpret_cast<const uint4*>(src0 + ((size_t)u * maxb + b) * B * D);
-    uint4* dst = reinterpret_cast<uint4*>(slots + ((size_t)u * cap + s) * B * D);
-    dst[tid] = src[tid];  // 256 threads x 16 B = one 4 KB block
+  // PCIe reads of zero-copy host memory are latency-bound: every thread keeps
+  // PI_DEPTH 16-byte loads (from PI_DEPTH different blocks) in flight
+  constexpr int PI_DEPTH = 8;
+  for (int k0 = 0; k0 < n; k0 += PI_DEPTH) {
+    uint4 v[PI_DEPTH];
+    int sl[PI_DEPTH];
+#pragma unroll
+    for (int i = 0; i < PI_DEPTH; ++i) {
+      sl[i] = -1;
+      if (k0 + i < n) {
+        const int b = ml[k0 + i];
+        sl[i] = slot_of[b];
+        if (sl[i] >= 0) {  // evicted again later in the same step: pass B reads Tier-2
+          if (tid == 0 && !c.tier2_valid[(size_t)u * maxb + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
+          v[i] = reinterpret_cast<const uint4*>(src0 + ((size_t)u * maxb + b) * B * D)[tid];
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PI_DEPTH; ++i)
+      if (sl[i] >= 0)
+        reinterpret_cast<uint4*>(slots + ((size_t)u * cap + sl[i]) * B * D)[tid] = v[i];
   }
 }
 
