@@ -86,8 +86,14 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
     const int cb = kt * 32 + (lane & 3) * 4;
     const float4 sa = *reinterpret_cast<const float4*>(sig + cb);
     const float4 sb = *reinterpret_cast<const float4*>(sig + cb + 16);
-    const float4 xa = *reinterpret_cast<const float4*>(aux + cb);
-    const float4 xb = *reinterpret_cast<const float4*>(aux + cb + 16);
+    // even lanes sum |q| sigma (sigma already loaded); only odd lanes load z --
+    // the shared-memory data pipe is pass A's bottleneck, predicated-off lanes
+    // cost no wavefronts
+    float4 xa = sa, xb = sb;
+    if (odd) {
+      xa = *reinterpret_cast<const float4*>(aux + cb);
+      xb = *reinterpret_cast<const float4*>(aux + cb + 16);
+    }
     const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
     const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
     uint32_t y[8];
