@@ -93,7 +93,10 @@ __device__ __forceinline__ void pv_block_sub(float (&acc)[NG][4], float (&accz)[
   mma_f16r(accz, oz.x, 0u, oz.y, 0u, F.z0, F.z1);
 }
 
-__global__ void __launch_bounds__(PA_WARPS * 32, 4) k_pass_a(StepArgs a) {
+#ifndef PA_MINB
+#define PA_MINB 4
+#endif
+__global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;

@@ -19,8 +19,7 @@
 namespace ckv {
 
 struct QFrag {
-  float qsc[32];   // q'_{h,c} * 2^(21-eQ_h) for h = lane/8, the lane's 32 channels
-  uint32_t amask;  // odd (lane/4): all ones (qsc, for sum q' z); even: clears the sign (|qsc|, Delta)
+  float qsc[16];   // q'_{h,c} * 2^(21-eQ_h) for h = lane/8, the lane's half (4 per k-tile)
   int eq_l;        // exponent of head lane%4: max|q'_h| < 2^eq_l
 };
 
@@ -48,15 +47,11 @@ __device__ inline void load_qfrag(QFrag& f, const float* qh, int lane) {
     if (h == hb) eq_b = e;
   }
   const float sc = pow2f(21 - eq_b);
-  const bool odd = (lane >> 2) & 1;
-  f.amask = odd ? 0xffffffffu : 0x7fffffffu;
+  const int half = (lane >> 2) & 1;
 #pragma unroll
   for (int kt = 0; kt < 4; ++kt) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float v = qh[hb * D + bchan(lane, kt, j)] * sc;
-      f.qsc[kt * 8 + j] = v;
-    }
+    for (int i = 0; i < 4; ++i) f.qsc[kt * 4 + i] = qh[hb * D + bchan(lane, kt, 4 * half + i)] * sc;
   }
 }
 
@@ -71,7 +66,6 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
   const float* sig = reinterpret_cast<const float*>(rec + OFF_KSCALE);
   const float* zz = reinterpret_cast<const float*>(rec + OFF_KOFF);
   const bool odd = (lane >> 2) & 1;
-  const float* aux = odd ? zz : sig;  // per-lane operand for the Delta / constz sums
   const int es = ilogbf(smax) + 1;    // smax < 2^es
   // fma(qsc, sigma, 1.5*2^(23+es)) has the same mantissa bits as
   // fma(qsc, sigma*2^-es, 1.5*2^23) (exact power-of-two scaling): the bytes of
@@ -79,35 +73,38 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
   // LSB (es & 1) in its top bit, removed below with the sum-of-codes column.
   const float magic_b = __uint_as_float(((uint32_t)(150 + es) << 23) | 0x400000u);
   const uint32_t sel0 = ((lane >> 2) & 1) ? 0x5151u : 0x4040u;  // byte 1 or 0 of y0,y1
+  // Lanes l and l^4 (byte parity of the same head) share their y values: each
+  // computes 4 of the 8 channels of a k-tile (one 16-byte sigma / z load each
+  // instead of two) and they swap halves with a shuffle.  The shared-memory
+  // data pipe is pass A's bottleneck.  Delta and sum q z partials are taken
+  // over the lane's own 4 channels and reduced over the 8 lanes of the head.
+  const int half = (lane >> 2) & 1;
   int d0[4] = {0, 0, 0, 0}, d1[4] = {0, 0, 0, 0};
-  float acc = 0.f;
+  float dacc = 0.f, zacc = 0.f;
 #pragma unroll
   for (int kt = 0; kt < 4; ++kt) {
-    const int cb = kt * 32 + (lane & 3) * 4;
-    const float4 sa = *reinterpret_cast<const float4*>(sig + cb);
-    const float4 sb = *reinterpret_cast<const float4*>(sig + cb + 16);
-    // even lanes sum |q| sigma (sigma already loaded); only odd lanes load z --
-    // the shared-memory data pipe is pass A's bottleneck, predicated-off lanes
-    // cost no wavefronts
-    float4 xa = sa, xb = sb;
-    if (odd) {
-      xa = *reinterpret_cast<const float4*>(aux + cb);
-      xb = *reinterpret_cast<const float4*>(aux + cb + 16);
-    }
-    const float sv[8] = {sa.x, sa.y, sa.z, sa.w, sb.x, sb.y, sb.z, sb.w};
-    const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    uint32_t y[8];
+    const int cm = kt * 32 + (lane & 3) * 4 + 16 * half;  // my 4 channels
+    const float4 s4 = *reinterpret_cast<const float4*>(sig + cm);
+    const float4 z4 = *reinterpret_cast<const float4*>(zz + cm);
+    const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+    const float zv[4] = {z4.x, z4.y, z4.z, z4.w};
+    uint32_t ym[4], yo[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      y[j] = __float_as_uint(fmaf(f.qsc[kt * 8 + j], sv[j], magic_b));
-      acc = fmaf(__uint_as_float(__float_as_uint(f.qsc[kt * 8 + j]) & f.amask), xv[j], acc);
+    for (int i = 0; i < 4; ++i) {
+      const float q = f.qsc[kt * 4 + i];
+      ym[i] = __float_as_uint(fmaf(q, sv[i], magic_b));
+      dacc = fmaf(fabsf(q), sv[i], dacc);
+      zacc = fmaf(q, zv[i], zacc);
     }
-    // tile 0: byte (lane/4)&1 of the four U values, packed into one register
-    uint32_t b00 = __byte_perm(__byte_perm(y[0], y[1], sel0), __byte_perm(y[2], y[3], sel0), 0x5410);
-    uint32_t b01 = __byte_perm(__byte_perm(y[4], y[5], sel0), __byte_perm(y[6], y[7], sel0), 0x5410);
-    // tile 1: byte 2 (even lane/4) or the ones column (odd lane/4)
-    uint32_t b10 = __byte_perm(__byte_perm(y[0], y[1], 0x6262u), __byte_perm(y[2], y[3], 0x6262u), 0x5410);
-    uint32_t b11 = __byte_perm(__byte_perm(y[4], y[5], 0x6262u), __byte_perm(y[6], y[7], 0x6262u), 0x5410);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) yo[i] = __shfl_xor_sync(0xffffffffu, ym[i], 4);
+    // byte planes of my half (m) and the partner's half (o)
+    const uint32_t pm0 = __byte_perm(__byte_perm(ym[0], ym[1], sel0), __byte_perm(ym[2], ym[3], sel0), 0x5410);
+    const uint32_t po0 = __byte_perm(__byte_perm(yo[0], yo[1], sel0), __byte_perm(yo[2], yo[3], sel0), 0x5410);
+    const uint32_t pm2 = __byte_perm(__byte_perm(ym[0], ym[1], 0x6262u), __byte_perm(ym[2], ym[3], 0x6262u), 0x5410);
+    const uint32_t po2 = __byte_perm(__byte_perm(yo[0], yo[1], 0x6262u), __byte_perm(yo[2], yo[3], 0x6262u), 0x5410);
+    const uint32_t b00 = half ? po0 : pm0, b01 = half ? pm0 : po0;
+    uint32_t b10 = half ? po2 : pm2, b11 = half ? pm2 : po2;
     if (odd) {
       b10 = 0x01010101u;
       b11 = 0x01010101u;
@@ -116,12 +113,15 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
     mma_s8u8(d0, a, b00, b01);
     mma_s8u8(d1, a, b10, b11);
   }
-  // reduce the Delta / constz partials over the 4 lanes sharing lane/4
-  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  // reduce over the 8 lanes of head lane/8, then fetch head lane%4's sums
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    dacc += __shfl_xor_sync(0xffffffffu, dacc, o);
+    zacc += __shfl_xor_sync(0xffffffffu, zacc, o);
+  }
   const int h = lane & 3;
-  const float dsum = __shfl_sync(0xffffffffu, acc, h * 8);      // sum |qsc| sigma (head h)
-  const float zsum = __shfl_sync(0xffffffffu, acc, h * 8 + 4);  // sum qsc z (head h)
+  const float dsum = __shfl_sync(0xffffffffu, dacc, h * 8);  // sum |qsc| sigma (head h)
+  const float zsum = __shfl_sync(0xffffffffu, zacc, h * 8);  // sum qsc z (head h)
   const float inv_q = pow2f(f.eq_l - 21);
   const float scl = pow2f(f.eq_l + es - 21);
   const float constz = zsum * inv_q;
