@@ -118,7 +118,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
   const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
   // Per-item metadata is software-pipelined so no dependent global load sits
-  // on the critical path: work entries are read two items ahead, the slot /
+  // on the critical path: work entries are read three items ahead, the slot /
   // key-scale / eta / Tier-2-valid words of an item one iteration before its
   // TMA is issued (the item after that) and consumed.
   struct Meta {
@@ -148,8 +148,10 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   };
   int cur = item_at(0);
   int i1 = item_at(1);
+  int i2 = item_at(2);
   Meta mc = load_meta(cur >= 0 ? work[cur] : 0, cur >= 0);
   Meta mn = load_meta(i1 >= 0 ? work[i1] : 0, i1 >= 0);
+  int e2 = (i2 >= 0) ? work[i2] : 0;  // work entry of item k+2 (read one iteration ahead)
   if (lane == 0 && cur >= 0) {
     fence_proxy_async();
     issue(mc, kb & 1);
@@ -158,8 +160,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   for (; cur >= 0; ++k) {
     const int stg = (kb + k) & 1;
     const int nxt = i1;
-    const int i2 = item_at(k + 2);
-    const int e_nn = (i2 >= 0) ? work[i2] : 0;  // consumed at the end of this iteration
+    const int i3 = item_at(k + 3);
+    const int e3 = (i3 >= 0) ? work[i3] : 0;  // consumed in the next iteration
     if (lane == 0 && nxt >= 0) {
       fence_proxy_async();
       issue(mn, stg ^ 1);
@@ -277,7 +279,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     cur = nxt;
     i1 = i2;
     mc = mn;
-    mn = load_meta(e_nn, i2 >= 0);
+    mn = load_meta(e2, i2 >= 0);
+    i2 = i3;
+    e2 = e3;
   }
   kb += k;
 
