@@ -333,7 +333,10 @@ struct SelSmem {
 };
 
 template <int KPT>
-__global__ void __launch_bounds__(SEL_THREADS, 2) k_select(StepArgs a) {
+#ifndef SEL_MINB
+#define SEL_MINB 4  // 64 registers (some spills) but 32 warps per SM: measured faster than 2
+#endif
+__global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
   uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
