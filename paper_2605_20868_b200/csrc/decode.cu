@@ -648,12 +648,14 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   // (all keys > T, plus the first `take` keys == T in block order)
   // this thread's eta values, vector-loaded up front (one latency, not KPT)
   const float* eta = c.eta + (size_t)u * c.max_blocks;
-  float etv[KPT];
-#pragma unroll
-  for (int j = 0; j < KPT; ++j) etv[j] = (BJ(j) < nb) ? __ldg(eta + BJ(j)) : 0.f;
   const float lse2 = lsef * 1.4426950408889634f;
   uint32_t gT = 0xffffffffu;
   int take = 0;
+  float etv[KPT];  // greedy mode only (the threshold path loads eta in chunks)
+  if (greedy) {
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) etv[j] = (BJ(j) < nb) ? __ldg(eta + BJ(j)) : 0.f;
+  }
   if (greedy && nb > 0) {
     double tot = 0.0;
 #pragma unroll
@@ -722,12 +724,22 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
       account(j, valid, pf, pe, inV);
     }
   } else {
+    // eta in chunks of 8 blocks per thread: bounded register pressure (the
+    // memory clobber keeps the compiler from hoisting every load to the top)
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const bool valid = BJ(j) < nb;
-      const float pf = valid ? ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) : 0.f;
-      const float pe = pf * etv[j];
-      account(j, valid, pf, pe, r2 && valid && (pe > vtol));
+    for (int j0 = 0; j0 < KPT; j0 += 8) {
+      float ev[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) ev[jj] = (BJ(j0 + jj) < nb) ? __ldg(eta + BJ(j0 + jj)) : 0.f;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int j = j0 + jj;
+        const bool valid = BJ(j) < nb;
+        const float pf = valid ? ex2_approx(fmaf(ukey(kk[j]), 1.4426950408889634f, -lse2)) : 0.f;
+        const float pe = pf * ev[jj];
+        account(j, valid, pf, pe, r2 && valid && (pe > vtol));
+      }
+      asm volatile("" ::: "memory");
     }
   }
   double at = (double)atf, et = (double)etf;
