@@ -247,7 +247,7 @@ def main():
     if args.kv_heads % world:
         raise SystemExit("kv_heads must be divisible by the number of GPUs")
     U = total_units // world
-    max_tokens = args.ctx + 2 * (K + W) + 32
+    max_tokens = args.ctx + 2 * (K + W) + max(K, 40) + 64  # timed + e2e appends
     cache = ck.DeviceKVCache(U, max_tokens, device=dev, tier2=args.tier2)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     chunk = max(16, min(4096, (1 << 22) // U))
@@ -377,9 +377,12 @@ def main():
     # ---- end to end through the public API with host buffers -----------------
     e2e = None
     if not args.no_e2e:
-        qh = torch.randn((K, U, args.q_per_kv, 128), dtype=torch.float64).pin_memory()
-        kh = torch.randn((K, U, 1, 128)).half().pin_memory()
-        vh = torch.randn((K, U, 1, 128)).half().pin_memory()
+        # steady state over E >= K steps (the one-step pipeline fill / drain amortised);
+        # NP pinned input sets cycled
+        E, NP = max(K, 40), min(max(K, 40), 8)
+        qh = torch.randn((NP, U, args.q_per_kv, 128), dtype=torch.float64).pin_memory()
+        kh = torch.randn((NP, U, 1, 128)).half().pin_memory()
+        vh = torch.randn((NP, U, 1, 128)).half().pin_memory()
         oh = torch.empty((U, args.q_per_kv, 128), dtype=torch.float32).pin_memory()
         for i in range(2):  # warm the pinned paths
             dec.step(qh[i].to(dev, non_blocking=True))
@@ -387,20 +390,25 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        kd = torch.empty((U, 1, 128), dtype=torch.float16, device=dev)
+        vd = torch.empty_like(kd)
         e0 = time.perf_counter()
         prev = None
-        for i in range(K):
-            p = dec.step_async(qh[i].to(dev, non_blocking=True), reduce_flags)
+        for i in range(E):
+            j = i % NP
+            dec.q.copy_(qh[j], non_blocking=True)            # H2D: this step's queries
+            p = dec.step_async(None, reduce_flags)          # + D2H of the certificates
             exchange()
-            oh.copy_(dec.out, non_blocking=True)
-            cache.append(kh[i].to(dev, non_blocking=True), vh[i].to(dev, non_blocking=True),
-                         validate="defer")
+            oh.copy_(dec.out, non_blocking=True)             # D2H: the attention outputs
+            kd.copy_(kh[j], non_blocking=True)               # H2D: the step's new token
+            vd.copy_(vh[j], non_blocking=True)
+            cache.append(kd, vd, validate="defer")
             if prev is not None:
                 prev.result()  # host reads step i-1's bound report while step i runs
             prev = p
         torch.cuda.synchronize()
         prev.result()
-        e_ms = (time.perf_counter() - e0) * 1000.0 / K
+        e_ms = (time.perf_counter() - e0) * 1000.0 / E
         if world > 1:
             t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -408,7 +416,7 @@ def main():
         h2d = qh[0].numel() * 8 + kh[0].numel() * 2 + vh[0].numel() * 2
         d2h = oh.numel() * 4 + dec.cert_buf.numel()
         e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": E}
 
     if rank != 0:
         if world > 1:
