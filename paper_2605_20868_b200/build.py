@@ -28,13 +28,20 @@ def needs_build():
 def build(force=False, verbose=False):
     if not force and not needs_build():
         return LIB
-    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    extra = os.environ.get("CKV_NVCC_EXTRA", "").split()  # experiments only (e.g. -DPA_MINB=4)
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *sources(), "-o", LIB + ".tmp"]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
+    import fcntl
+    # one builder at a time (e.g. every rank of a torchrun job calling build())
+    with open(LIB + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not needs_build():  # another process built it meanwhile
+            return LIB
+        nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+        extra = os.environ.get("CKV_NVCC_EXTRA", "").split()  # experiments only (e.g. -DPA_MINB=4)
+        tmp = f"{LIB}.{os.getpid()}.tmp"
+        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB)
     return LIB
 
 
