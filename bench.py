@@ -195,6 +195,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knob for exercising the sharded path on a single GPU (every rank on cuda:0, gloo)
+    if os.environ.get("CKV_BENCH_ONE_DEVICE"):
+        local = 0
     K, W = args.steps, max(3, args.warmup)
     total_units = args.layers * args.kv_heads * args.batch
     pol_desc = "PolicyConfig(exploration_rate=0.0) defaults"
@@ -235,7 +238,10 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("CKV_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import __graft_entry__
     __graft_entry__.build()
     import paper_2605_20868_b200 as ck
