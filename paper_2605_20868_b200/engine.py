@@ -12,6 +12,7 @@ for every (unit, q-head); the host then reads back the certificate array.
 
 import ctypes
 import dataclasses
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -125,6 +126,8 @@ class CertifiedDecoder:
                         ("dense_part", self.dense_part), ("explore_pos", self.explore_pos),
                         ("unit_done", self.unit_done)):
             setattr(st, name, _ptr(t))
+        if os.environ.get("CKV_SEPARATE_UNION"):  # A/B knob: union list by its own launch
+            st.unit_done = None
         # step-wide Rung 4 (harness.py:362-372) acts on groups of units: one
         # group = the reference's single step (None), contiguous runs of
         # ``rung4_group`` units (int), or explicit group ids per unit (array,
