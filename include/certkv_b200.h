@@ -165,6 +165,12 @@ typedef struct {
                                separate launch does) */
   int32_t* queue;           /* [2] zero-initialised, self-resetting work-queue counters of the
                                persistent pass B (NULL: one CTA per (chunk, unit)) */
+  float* stash;             /* [n_units][max_blocks][4][16] phase-1 scores of likely-promoted
+                               blocks, written by pass A (NULL: off) */
+  int32_t* stash_epoch;     /* [n_units][max_blocks] epoch << 4 | mask of stashed heads (init -1) */
+  int32_t epoch;            /* this step's epoch, < 2^27 (the caller increments it every step) */
+  float stash_margin;       /* a block is stashed when some head's l'_b exceeds that head's
+                               largest tail l' of the previous step minus this margin */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136

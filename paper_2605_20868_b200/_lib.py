@@ -64,7 +64,8 @@ class CkvStep(ctypes.Structure):
                 ("rung4_group", I32), ("n_dsplit_cap", I32), ("dense_list", P), ("dense_part", P),
                 ("ecap", I32), ("explore_n", P), ("explore_pos", P), ("unit_group", P),
                 ("group_flags", P), ("n_groups", I32), ("unit_done", P),
-                ("queue", P)]
+                ("queue", P), ("stash", P), ("stash_epoch", P), ("epoch", I32),
+                ("stash_margin", ctypes.c_float)]
 
 
 class CkvScratch(ctypes.Structure):

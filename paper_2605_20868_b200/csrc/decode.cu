@@ -150,6 +150,14 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   accz[0] = accz[1] = accz[2] = accz[3] = 0.f;
 
   float* lm1 = st.lm1 + ((size_t)u * nh + (h < nh ? h : 0)) * c.max_blocks;
+  // stash threshold of this lane's head: the previous step's largest tail l' minus a
+  // margin (+inf before the first step or without a stash)
+  float sthr = __int_as_float(0x7f800000);
+  if (st.stash && h < nh) {
+    const HeadState& hp = *reinterpret_cast<const HeadState*>(st.head_state + ((size_t)u * nh + h) * CKV_HEAD_FLOATS);
+    if (hp.kprime > 0) sthr = hp.tailmax - st.stash_margin;
+  }
+  float* stash_u = st.stash ? st.stash + (size_t)u * c.max_blocks * 64 : nullptr;
 
   float smax_nxt = (nmine > 0) ? __ldg(smax_u + b0 + warp) : 0.f;
   for (int i = 0; i < nmine; ++i) {
@@ -172,7 +180,21 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     bs += __shfl_xor_sync(0xffffffffu, bs, 4);
     bs += __shfl_xor_sync(0xffffffffu, bs, 8);
     bs += __shfl_xor_sync(0xffffffffu, bs, 16);
-    if (lane < nh) lm1[b] = bm + __logf(bs);
+    bool cand = false;
+    if (lane < nh) {
+      const float lb = bm + __logf(bs);
+      lm1[b] = lb;
+      cand = lb > sthr;
+    }
+    // likely promoted for some head: keep that head's scores for pass B
+    const uint32_t smask = stash_u ? (__ballot_sync(0xffffffffu, cand) & 0xfu) : 0u;
+    if (smask) {
+      if ((smask >> h) & 1u) {
+        stash_u[(size_t)b * 64 + h * 16 + t0] = r.s0;
+        stash_u[(size_t)b * 64 + h * 16 + t0 + 8] = r.s1;
+      }
+      if (lane == 0) st.stash_epoch[(size_t)u * c.max_blocks + b] = (st.epoch << 4) | (int)smask;
+    }
     dmax = fmaxf(dmax, r.delta);
     const float m_new = fmaxf(m_run, bm);
     const float alpha = fast_exp(m_run - m_new);

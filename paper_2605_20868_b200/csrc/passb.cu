@@ -33,6 +33,7 @@ struct PassBSmem {
   uint8_t rec[PB_WARPS][2][REC];
   uint8_t kt[PB_WARPS][2][B * D * 2];  // FP16 Tier-2 key tile (fragment order) of promoted blocks
   uint64_t bar[PB_WARPS][2];
+  float sst[PB_WARPS][2][H * B];  // stashed phase-1 scores of the item (pass A), [head][token]
   float qh[H * D];
   float cq[PB_WARPS][H][B];  // coefficient of v_hat per (head, token), tokens permuted
   float ca[PB_WARPS][H][B];  // coefficient of the original v
@@ -122,9 +123,10 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   // key-scale / eta / Tier-2-valid words of an item one iteration before its
   // TMA is issued (the item after that) and consumed.
   struct Meta {
-    int e, sl, valid;
+    int e, sl, valid, st;
     float smax, eta;
   };
+  const float* stash_u = st.stash ? st.stash + (size_t)u * c.max_blocks * 64 : nullptr;
   auto load_meta = [&](int e2, bool ok) -> Meta {  // work entries may have bit 31 set
     Meta m;
     m.e = e2;
@@ -133,13 +135,28 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     m.smax = ok ? c.kscale_max[ubk + b2] : 1.f;
     m.eta = ok ? eta[b2] : 0.f;
     m.valid = ok ? c.tier2_valid[ubk + b2] : 1;
+    // usable when this step's pass A stashed every head the item is promoted for
+    if (ok && stash_u) {
+      const int se = st.stash_epoch[ubk + b2];
+      const uint32_t need = (((uint32_t)e2 >> 24) | ((uint32_t)e2 >> 28)) & 0xfu;
+      m.st = ((se >> 4) == st.epoch) && ((need & ~(uint32_t)se) == 0u);
+    } else {
+      m.st = 0;
+    }
     return m;
   };
   auto issue = [&](const Meta& m, int stg) {
     const int b2 = m.e & 0xffffff;
     const bool keys = ((uint32_t)m.e >> 24) & 0xfu;
-    mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
-    bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
+    if (m.st) {  // scores stashed by pass A: only the value part of the record (+ the stash)
+      mbar_expect_tx(&S.bar[warp][stg], (REC - OFF_VCODES) + H * B * 4 + (keys ? B * D * 2 : 0));
+      bulk_g2s(S.rec[warp][stg] + OFF_VCODES, t1base + (size_t)b2 * REC + OFF_VCODES, REC - OFF_VCODES,
+               &S.bar[warp][stg]);
+      bulk_g2s(S.sst[warp][stg], stash_u + (size_t)b2 * 64, H * B * 4, &S.bar[warp][stg]);
+    } else {
+      mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
+      bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
+    }
     if (keys) {
       const uint16_t* src = (m.sl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
                                         : c.tier2_k + (ubk + b2) * B * D;
@@ -176,7 +193,16 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
     const uint8_t* rec = S.rec[warp][stg];
 
-    const BlockScores r = phase1_block(f, rec, smax, lane);
+    BlockScores r;
+    if (mc.st) {  // bit-identical to phase1_block in pass A (that is where they come from)
+      // heads the item is not promoted for have no stash entry and take no part
+      const bool need_h = ((fm | vm) >> h) & 1u;
+      r.s0 = need_h ? S.sst[warp][stg][h * B + t0] : ninf();
+      r.s1 = need_h ? S.sst[warp][stg][h * B + t0 + 8] : ninf();
+      r.delta = 0.f;
+    } else {
+      r = phase1_block(f, rec, smax, lane);
+    }
     float sn0 = r.s0, sn1 = r.s1;
     if (fm) {
       const float2 so = orig_block(f16, reinterpret_cast<const uint4*>(S.kt[warp][stg]), lane);

@@ -128,6 +128,16 @@ class CertifiedDecoder:
             setattr(st, name, _ptr(t))
         if os.environ.get("CKV_SEPARATE_UNION"):  # A/B knob: union list by its own launch
             st.unit_done = None
+        # phase-1 score stash: pass A keeps the quantized scores of blocks likely to be
+        # promoted (predicted from the previous step's tail threshold) so pass B needs
+        # only the value part of their Tier-1 record (exact either way)
+        if not os.environ.get("CKV_NO_STASH"):
+            self.stash = torch.empty((U, NB, 4 * 16), dtype=torch.float32, device=dev)
+            self.stash_epoch = torch.full((U, NB), -1, dtype=torch.int32, device=dev)
+            st.stash = _ptr(self.stash)
+            st.stash_epoch = _ptr(self.stash_epoch)
+            st.stash_margin = float(os.environ.get("CKV_STASH_MARGIN", "0.1"))
+        st.epoch = 0
         # step-wide Rung 4 (harness.py:362-372) acts on groups of units: one
         # group = the reference's single step (None), contiguous runs of
         # ``rung4_group`` units (int), or explicit group ids per unit (array,
@@ -167,6 +177,7 @@ class CertifiedDecoder:
         sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
         args = (ctypes.byref(self.cache.c), ctypes.byref(self.pol_c), ctypes.byref(self.st))
         nbk, stream = self.cache.num_blocks, _stream(self.cache.device)
+        self.st.epoch = (self.st.epoch + 1) & 0x3ffffff
         if reduce_flags is None:
             _lib.check(self.lib.ckv_decode_step(*args, sc, nbk, stream), "ckv_decode_step")
             return
@@ -258,6 +269,7 @@ class CertifiedDecoder:
         stream = _stream(self.cache.device)
         nbk = self.cache.num_blocks
         sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
+        self.st.epoch = (self.st.epoch + 1) & 0x3ffffff
         _lib.check(self.lib.ckv_decode_begin(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
                                              ctypes.byref(self.st), sc, nbk, stream), "ckv_decode_begin")
         self.cert_host.copy_(self.cert_buf, non_blocking=True)

@@ -38,7 +38,7 @@ def test_struct_layouts():
     assert ctypes.sizeof(_lib.CkvCert) == 8 * 8 + 6 * 4
     assert ctypes.sizeof(_lib.CkvPolicy) == 4 * 8 + 8 * 4
     assert ctypes.sizeof(_lib.CkvCache) == 8 + 13 * 8
-    assert ctypes.sizeof(_lib.CkvStep) == 7 * 4 + 4 + 15 * 8 + 2 * 4 + 2 * 8 + 8 + 2 * 8 + 2 * 8 + 8 + 8 + 8
+    assert ctypes.sizeof(_lib.CkvStep) == 7 * 4 + 4 + 15 * 8 + 2 * 4 + 2 * 8 + 8 + 2 * 8 + 2 * 8 + 8 + 8 + 8 + 2 * 8 + 4 + 4
     assert ctypes.sizeof(_lib.CkvScratch) == 8 + 7 * 8 + 8
 
 
