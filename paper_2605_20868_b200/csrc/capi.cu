@@ -79,7 +79,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->n_chunks = (4 * st->kcap + 127) / 128;
   if (st->n_chunks < 1) st->n_chunks = 1;
   if (st->n_chunks > 256) st->n_chunks = 256;
-  st->n_dsplit_cap = (max_blocks * CKV_BLOCK + CKV_BLOCK + 2047) / 2048;
+  st->n_dsplit_cap = max_blocks / 8 < 1 ? 1 : (max_blocks / 8 > 256 ? 256 : max_blocks / 8);  /* dense splits per unit */
   return CKV_OK;
 }
 

@@ -13,15 +13,18 @@
 
 namespace ckv {
 
-constexpr int DN_TOK = 2048;  // tokens per dense split
+constexpr int DN_MAXSPLIT = 256;  // splits per dense unit (merge buffer)
+#ifndef DN_SPLITS
+#define DN_SPLITS 128
+#endif
 constexpr int DN_WARPS = 4;
 
 struct DenseArgs {
   ckv_cache c;
   ckv_step st;
-  int32_t group;     // units per rung-4 group
-  int32_t n_dsplit;  // splits per unit
-  int32_t blk_per_split;
+  int32_t group;     // (unused)
+  int32_t n_dsplit;  // splits per dense unit of this launch (set on device from the count)
+  int32_t blk_per_split;  // (unused)
 };
 
 __device__ __forceinline__ float dninf() { return __int_as_float(0xff800000); }
@@ -73,9 +76,9 @@ __device__ void dense_merge_item(const DenseArgs& a, int item) {
   const int tid = threadIdx.x;
   const int pl = c.partial_len[u];
   const int ns = a.n_dsplit;
-  __shared__ float sm_m[H][160], sm_sc[H][160];
+  __shared__ float sm_m[H][DN_MAXSPLIT], sm_sc[H][DN_MAXSPLIT];
   __shared__ float red[H][4];
-  const float* p0 = st.dense_part + ((size_t)item * ns * H) * 132;
+  const float* p0 = st.dense_part + ((size_t)item * st.n_dsplit_cap * H) * 132;
   // per-split maxima -> per-head frame, splits spread over the threads
   for (int i = tid; i < ns * H; i += blockDim.x) sm_m[i % H][i / H] = __ldcg(p0 + (size_t)i * 132);
   __syncthreads();
@@ -145,25 +148,35 @@ struct DenseSmem {
 // tensor cores too: A = the fragment-ordered FP16 values (exact), B = the
 // weights as an fp16 hi/lo pair (column 2h + part), fp32 accumulation.  The
 // partial block is added in the merge from the state k_select computed.
-__global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
+__global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   __shared__ __align__(16) DenseSmem S;
   __shared__ __align__(16) float ow[DN_WARPS][H][D];
   __shared__ float mw[DN_WARPS][H][2];
+  DenseArgs a = a_in;
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
-  const int item = blockIdx.y, sp = blockIdx.x;
-  if (item >= st.dense_list[0]) return;
+  // persistent over (item, split) tasks; the split count adapts to the number of
+  // dense units so that a few of them still spread over every SM
+  const int count = st.dense_list[0];
+  if (count == 0) return;
+  // ~384 tasks in all: long splits (little merge work) when many units are dense,
+  // up to DN_SPLITS per unit when only a few are (latency-bound otherwise)
+  a.n_dsplit = min(st.n_dsplit_cap, min(DN_SPLITS, max(32, (384 + count - 1) / count)));
+  for (int task = blockIdx.x; task < count * a.n_dsplit; task += gridDim.x) {
+  const int item = task / a.n_dsplit, sp = task % a.n_dsplit;
   const int e = st.dense_list[1 + c.n_units + item];
   const int u = e & 0xffffff;
   const int nh = st.n_heads;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nb = c.n_blocks[u];
-  const int b0 = sp * a.blk_per_split, b1 = min(nb, b0 + a.blk_per_split);
-  float* outp = st.dense_part + (((size_t)item * a.n_dsplit + sp) * H) * 132;
+  const int bps = max(1, (nb + a.n_dsplit - 1) / a.n_dsplit);
+  const int b0 = sp * bps, b1 = min(nb, b0 + bps);
+  float* outp = st.dense_part + (((size_t)item * st.n_dsplit_cap + sp) * H) * 132;
+  __syncthreads();  // the previous task is done with S / ow / mw
   if (b0 >= b1) {
     for (int i = tid; i < H * 132; i += blockDim.x) outp[i] = (i % 132 == 0) ? dninf() : 0.f;
     dense_split_done(a, item);
-    return;
+    continue;
   }
   for (int i = tid; i < H * D; i += blockDim.x) {
     const int h = i / D;
@@ -249,6 +262,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a) {
     outp[hh * 132 + 4 + tid] = O;
   }
   dense_split_done(a, item);
+  }  // task loop
 }
 
 extern int g_launches;
@@ -263,17 +277,19 @@ cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStrea
 }
 
 cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_tokens, cudaStream_t s) {
-  DenseArgs a{*c, *st, 0, 0, DN_TOK / B};
-  // full blocks only (the partial block comes from the head state); at most
-  // 160 splits so the merge fits its shared buffers
-  const int nblk = (host_max_tokens + B - 1) / B;
-  while ((nblk + a.blk_per_split - 1) / a.blk_per_split > 160) a.blk_per_split *= 2;
-  a.n_dsplit = (nblk + a.blk_per_split - 1) / a.blk_per_split;
-  if (a.n_dsplit < 1) a.n_dsplit = 1;
-  if (a.n_dsplit > st->n_dsplit_cap) a.n_dsplit = st->n_dsplit_cap;
+  (void)host_max_tokens;
+  DenseArgs a{*c, *st, 0, 1, 0};
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dense, DN_WARPS * 32, 0);
+    slots = max(1, sms * max(1, per));
+  }
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t) * (1 + c->n_units), s);  // count + done counters
   k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
-  k_dense<<<dim3(a.n_dsplit, c->n_units), DN_WARPS * 32, 0, s>>>(a);
+  k_dense<<<slots, DN_WARPS * 32, 0, s>>>(a);
   g_launches += 2;
   return cudaGetLastError();
 }
