@@ -193,6 +193,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// L2 prefetch of a global range by the TMA unit (no registers, no shared memory)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const char* c = reinterpret_cast<const char*>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15);
+  const char* e = reinterpret_cast<const char*>(p) + bytes;
+  while (c < e) {
+    const uint32_t n = (uint32_t)min((long long)(e - c + 15) & ~15ll, 16384ll);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(n) : "memory");
+    c += n;
+  }
+}
+
 // ---- cp.async (LDGSTS) ------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");

@@ -354,11 +354,29 @@ struct SelSmem {
   float redf[40];
 };
 
+// Phase profile of k_select (build with -DCKV_SELPROF; tools/selprof.py): thread 0
+// of every CTA adds globaltimer deltas between barrier-fenced markers.
+#ifdef CKV_SELPROF
+__device__ unsigned long long g_selprof[16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+#define SELPROF(i) do { __syncthreads(); if (threadIdx.x == 0) { unsigned long long t_ = gtimer(); atomicAdd(&g_selprof[i], t_ - t_prev); t_prev = t_; } __syncthreads(); } while (0)
+extern "C" void ckv_debug_selprof(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_selprof, sizeof(g_selprof)); }
+#else
+#define SELPROF(i) do {} while (0)
+#endif
+
 template <int KPT>
 #ifndef SEL_MINB
 #define SEL_MINB 4  // 64 registers (some spills) but 32 warps per SM: measured faster than 2
 #endif
 __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
+#ifdef CKV_SELPROF
+  unsigned long long t_prev = gtimer();
+#endif
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
   uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
@@ -374,6 +392,13 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   const float* lm = st.lm1 + hu * c.max_blocks;
   HeadState& hs = *reinterpret_cast<HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
 
+  // the eta annotations (tail pass) and this head's pass-A split states (merge) are
+  // needed later: start pulling them into L2 now
+  if (tid == 0) {
+    prefetch_l2(c.eta + (size_t)u * c.max_blocks, (uint32_t)nb * 4u);
+    prefetch_l2(st.split_state + (size_t)u * st.n_splits * H * CKV_SPLIT_FLOATS,
+                (uint32_t)((nb + st.blocks_per_split - 1) / st.blocks_per_split) * H * CKV_SPLIT_FLOATS * 4u);
+  }
   // ---- this thread's blocks tid + SEL_THREADS * j (j < KPT): order keys of l'_b in
   // registers; strided ownership keeps every load coalesced
 #define BJ(j) (tid + SEL_THREADS * (j))
@@ -385,6 +410,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   for (int i = tid; i < (c.max_blocks + 31) / 32; i += SEL_THREADS) fmask[i] = 0u;
   __syncthreads();
 
+  SELPROF(1);
   // ---- partial block on originals (attention.py:98-104) ------------------------
   for (int t = warp; t < pl; t += SEL_THREADS / 32) {
     const uint16_t* pk = c.partial_k + ((size_t)u * B + t) * D;
@@ -408,6 +434,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     hs.np_[tid] = acc;
   }
 
+  SELPROF(2);
   // ---- merge the pass-A splits: headers in parallel, then independent loads ---------
   const int nsp = (nb + st.blocks_per_split - 1) / st.blocks_per_split;
   {
@@ -446,6 +473,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     __syncthreads();
   }
 
+  SELPROF(3);
   // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
   float lmax = lmp;
 #pragma unroll
@@ -462,6 +490,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   const float lsef = (float)lse;
   const double pmass = (pl > 0) ? exp((double)lmp - lse) : 0.0;
 
+  SELPROF(4);
   // ---- top K_sel blocks by l' (ties -> lower index) -------------------------------
   // T = the K_sel-th largest key by a 3-digit (11/11/10 bit) radix select over
   // shared histograms, then the candidates (all keys > T, the first keys == T
@@ -611,6 +640,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     __syncthreads();
   }
 
+  SELPROF(5);
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
   for (int i = tid; i < n_sorted; i += SEL_THREADS) {
     S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
@@ -662,6 +692,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   }
   __syncthreads();
 
+  SELPROF(6);
   // ---- tail mass, rung 2, E_val tail (fallback.py:141-161, certifier.py:153-160) ----
   const bool r2 = pol.rung2_enabled != 0;
   const bool greedy = r2 && pol.greedy_value_budget >= 0.0;
@@ -799,6 +830,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     if (kcov != kstar) fl |= CKV_F_CLAMPED;
     ct.flags = fl;
   }
+  SELPROF(7);
   // the last q-head of the unit to finish builds the unit's union work list
   if (st.unit_done) {
     __shared__ int last;
@@ -812,6 +844,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     }
     __syncthreads();
     if (last) build_union(c, st, u, reinterpret_cast<uint32_t*>(&S), S.wsum);
+    if (last) SELPROF(9);
   }
 }
 

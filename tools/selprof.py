@@ -11,7 +11,7 @@ cmd = ["nvcc", *build.NVCC_FLAGS, "-DCKV_SELPROF", "-I", os.path.join(ROOT, "inc
 subprocess.run(cmd, check=True)
 _lib.LIB_PATH = out
 import paper_2605_20868_b200 as ck
-units, ctx = int(os.environ.get("UNITS", "64")), int(os.environ.get("CTX", "131072"))
+units, ctx = int(os.environ.get("UNITS", "256")), int(os.environ.get("CTX", "131072"))
 dev = torch.device("cuda")
 cache = ck.DeviceKVCache(units, ctx + 64, device=dev)
 g = torch.Generator(device=dev).manual_seed(0)
