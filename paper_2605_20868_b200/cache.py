@@ -110,6 +110,12 @@ class DeviceKVCache:
     def num_tokens(self):
         return self._tokens
 
+    def resync(self):
+        """Re-read the token count from the device (after a deferred append was
+        rejected there, the host mirror counted tokens the device refused)."""
+        nb = int(self.n_blocks_t[0].item())
+        self._tokens = nb * B + int(self.partial_len_t[0].item())
+
     @property
     def num_blocks(self):
         return self._tokens // B

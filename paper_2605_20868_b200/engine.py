@@ -250,6 +250,7 @@ class CertifiedDecoder:
     def _output(self, cert_h, stat_h, ps_h, n_tokens):
         if stat_h[_lib.ST_NONFINITE]:  # a deferred append check (DeviceKVCache.append)
             self.cache.status[_lib.ST_NONFINITE] = 0
+            self.cache.resync()
             raise ValueError("non-finite key/value entry (append rejected on the device)")
         if stat_h[_lib.ST_TIER2]:
             self.cache.status[_lib.ST_TIER2] = 0

@@ -418,3 +418,40 @@ def test_adversarial_outliers_near_tie_fault(ck):
         if s == 2:
             assert (res.kinds[0] == 2).all()      # the corrupted unit's group is dense
             assert not (res.kinds[1] == 2).any()  # the other group is not
+
+
+# ---- serving-loop API ---------------------------------------------------------------
+
+def test_step_async_matches_step_and_defers_append_check(ck):
+    """step_async returns the same certificates as step (one step later on the
+    host); a non-finite append with validate="defer" is rejected on the device
+    and surfaces as ValueError from the next step's result."""
+    rng = np.random.default_rng(21)
+    U, n = 3, 700
+    k = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    v = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    ca = ck.DeviceKVCache(U, n + 32)
+    cb = ck.DeviceKVCache(U, n + 32)
+    ca.append(k, v)
+    cb.append(k, v)
+    pol = ck.PolicyConfig(exploration_rate=0.0, k_max=6)
+    da = ck.CertifiedDecoder(ca, pol, n_heads=4, rung4_group=[0, 1, 0])
+    db = ck.CertifiedDecoder(cb, pol, n_heads=4, rung4_group=[0, 1, 0])
+    qs = [torch.from_numpy(rng.standard_normal((U, 4, 128))).cuda() for _ in range(3)]
+    pend = []
+    for q in qs:
+        pend.append(da.step_async(q))
+        rb = db.step(q)
+        ra = pend[-1].result()
+        np.testing.assert_array_equal(ra.cert, rb.cert)
+        np.testing.assert_array_equal(da.out.cpu().numpy(), db.out.cpu().numpy())
+    bad = torch.full((U, 1, 128), float("nan"), dtype=torch.float16, device="cuda")
+    t0 = ca.num_tokens
+    pl0 = ca.partial_len_t.clone()
+    ca.append(bad, bad, validate="defer")
+    with pytest.raises(ValueError):
+        da.step_async(qs[0]).result()
+    assert torch.equal(ca.partial_len_t, pl0) and ca.num_tokens == t0  # nothing appended
+    ca.append(k[:, :1], v[:, :1], validate="defer")  # the cache keeps working
+    da.step_async(qs[1]).result()
+    assert ca.num_tokens == t0 + 1
