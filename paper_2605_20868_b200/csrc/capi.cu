@@ -75,8 +75,11 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->n_splits = (max_blocks + bps - 1) / bps;
   st->kcap = 2 * pol->k_max + 2;
   st->wcap = st->kcap + max_blocks;
-  st->items_per_chunk = 128;
-  st->n_chunks = (4 * st->kcap + 127) / 128;
+  st->items_per_chunk = 192;  /* measured at C3: 192 < 128 < 352 < 256 us */
+#ifdef CKV_PB_IPC
+  st->items_per_chunk = CKV_PB_IPC;
+#endif
+  st->n_chunks = (4 * st->kcap + st->items_per_chunk - 1) / st->items_per_chunk;
   if (st->n_chunks < 1) st->n_chunks = 1;
   if (st->n_chunks > 256) st->n_chunks = 256;
   st->n_dsplit_cap = max_blocks / 8 < 1 ? 1 : (max_blocks / 8 > 256 ? 256 : max_blocks / 8);  /* dense splits per unit */
