@@ -68,7 +68,10 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
       pol->ranking_depth < 1 || pol->ranking_depth > 64)
     return CKV_EINVAL;
   long long work = (long long)n_units * max_blocks / 1184;
-  int bps = 256;
+#ifndef CKV_PA_BPS
+#define CKV_PA_BPS 256
+#endif
+  int bps = CKV_PA_BPS;
   while (bps > 16 && bps > work) bps >>= 1;
   st->n_heads = n_heads;
   st->blocks_per_split = bps;

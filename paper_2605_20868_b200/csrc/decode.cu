@@ -499,7 +499,10 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   // with rung 1); the largest tail key comes from a reduction below
   const int kwant = pol.rung1_enabled ? 2 * pol.k_max : pol.k_max;
   const int ksel = min(nb, min(kwant, SEL_MAXSORT));
-  const int sort_cap = max(ksel, SEL_THREADS);  // one rank-sort round
+#ifndef SEL_SORTCAP
+#define SEL_SORTCAP 384
+#endif
+  const int sort_cap = max(ksel, SEL_SORTCAP);  // candidates allowed into the rank sort
   int n_sorted = 0;
   if (ksel > 0) {
     // digits of (key - min key), 11 bits at a time from the top of the occupied
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
         n_cand = above + binc;
       }
     }
+    SELPROF(8);
     const uint32_t T = kmn + prefix;
     if (!exact) {
       // candidates: every key >= T (the lower edge of the last bin), block order
@@ -622,8 +626,10 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
       n_sorted = ksel;
     }
     __syncthreads();
+    SELPROF(10);
     // rank sort (composite keys are distinct): position = #greater; the
-    // candidate list is read as broadcast 16-byte pairs
+    // candidate list is read as broadcast 16-byte pairs (a thread per candidate
+    // measured faster than warp-cooperative variants)
     for (int i = tid; i < n_sorted; i += SEL_THREADS) {
       const unsigned long long x = S.cand[i];
       int r = 0;

@@ -25,7 +25,7 @@ lib = _lib.load()
 buf = (ctypes.c_ulonglong * 16)()
 lib.ckv_debug_selprof(buf)
 n = units * 4 * 3
-names = {1: "keys+init", 2: "partial", 3: "split-merge", 4: "lse", 5: "top-K", 6: "coverage+order",
+names = {1: "keys+init", 2: "partial", 3: "split-merge", 4: "lse", 8: "radix", 10: "gather", 5: "rank sort", 6: "coverage+order",
          7: "tail/rung2/cert", 9: "union (last CTA)"}
 for i, nm in names.items():
     print(f"{nm:18s} {buf[i] / n / 1000:8.2f} us/CTA")
