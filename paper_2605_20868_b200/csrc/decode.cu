@@ -26,8 +26,14 @@ namespace ckv {
 // =============================================================================
 // pass A
 // =============================================================================
-constexpr int PA_WARPS = 4;
-constexpr int PA_STAGES = 2;
+#ifndef PA_WARPS_CFG
+#define PA_WARPS_CFG 4
+#endif
+#ifndef PA_STAGES_CFG
+#define PA_STAGES_CFG 2
+#endif
+constexpr int PA_WARPS = PA_WARPS_CFG;
+constexpr int PA_STAGES = PA_STAGES_CFG;
 
 struct PassASmem {
   uint8_t stage[PA_WARPS][PA_STAGES][REC];
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     ow[(warp * H + h) * D + c0 + 8] = fmaf(acc[g][2] + acc[g][3], 16777216.f, zg) * inv;
   }
   __syncthreads();
-  const int ch = tid;  // 128 threads = 128 channels
+  for (int ch = tid; ch < D; ch += PA_WARPS * 32) {
   for (int hh = 0; hh < H; ++hh) {
     float M = ninf(), dm = 0.f;
     for (int w = 0; w < PA_WARPS; ++w) {
@@ -271,6 +277,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
       outp[3] = 0.f;
     }
     outp[4 + ch] = O;
+  }
   }
 }
 
