@@ -236,7 +236,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
         canary = fmaxf(canary, gap);
         if (lane < H && h < nh) {
           lm2[b] = lb;
-          const double rb = exp((double)lb - lse);
+          const double rb = (double)__expf(lb - (float)lse);  // phase-2 block mass (fp32 exp: 1e-7 rel.)
           sF += rb;
           if (!inV) eF += rb * (double)eta_b;
         }
