@@ -922,7 +922,11 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   StepArgs a{*c, *st, *pol, PageView{}, u0};
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
-  if (nbh <= SEL_THREADS * 32)
+  if (nbh <= SEL_THREADS * 8)
+    k_select<8><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+  else if (nbh <= SEL_THREADS * 16)
+    k_select<16><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+  else if (nbh <= SEL_THREADS * 32)
     k_select<32><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 64)
     k_select<64><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
@@ -981,6 +985,8 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+    cudaFuncSetAttribute(k_select<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
