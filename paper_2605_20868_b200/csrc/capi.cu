@@ -79,6 +79,11 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   st->kcap = 2 * pol->k_max + 2;
   st->wcap = st->kcap + max_blocks;
   st->items_per_chunk = 192;  /* measured at C3: 192 < 128 < 352 < 256 us */
+  /* few units (e.g. 8-way KV-head sharding): smaller chunks so pass B still fills the GPU */
+  while (st->items_per_chunk > 32 &&
+         (long long)n_units * ((4 * st->kcap + st->items_per_chunk - 1) / st->items_per_chunk) < 888)
+    st->items_per_chunk /= 2;
+  if (st->items_per_chunk < 32) st->items_per_chunk = 32;
 #ifdef CKV_PB_IPC
   st->items_per_chunk = CKV_PB_IPC;
 #endif
