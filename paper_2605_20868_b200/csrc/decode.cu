@@ -299,14 +299,14 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
   if (lane == 31) wsum[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int w = (lane < SEL_THREADS / 32) ? wsum[lane] : 0;
+    int w = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    if (lane < SEL_THREADS / 32) wsum[lane] = w;
-    if (lane == SEL_THREADS / 32 - 1) *total = w;
+    if (lane < (int)(blockDim.x >> 5)) wsum[lane] = w;
+    if (lane == (int)(blockDim.x >> 5) - 1) *total = w;
   }
   __syncthreads();
   int before = (warp > 0) ? wsum[warp - 1] : 0;
@@ -322,11 +322,11 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
   __syncthreads();
   double t = 0.0;
   if (threadIdx.x == 0) {
-    for (int w = 0; w < SEL_THREADS / 32; ++w) t += red[w];
-    red[SEL_THREADS / 32] = t;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[(int)(blockDim.x >> 5)] = t;
   }
   __syncthreads();
-  t = red[SEL_THREADS / 32];
+  t = red[(int)(blockDim.x >> 5)];
   __syncthreads();
   return t;
 }
@@ -338,11 +338,11 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
   __syncthreads();
   if (threadIdx.x == 0) {
     float t = red[0];
-    for (int w = 1; w < SEL_THREADS / 32; ++w) t = fmaxf(t, red[w]);
-    red[SEL_THREADS / 32] = t;
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, red[w]);
+    red[(int)(blockDim.x >> 5)] = t;
   }
   __syncthreads();
-  float t = red[SEL_THREADS / 32];
+  float t = red[(int)(blockDim.x >> 5)];
   __syncthreads();
   return t;
 }
@@ -376,11 +376,11 @@ extern "C" void ckv_debug_selprof(unsigned long long* out) { cudaMemcpyFromSymbo
 #define SELPROF(i) do {} while (0)
 #endif
 
-template <int KPT>
+template <int KPT, int NT>
 #ifndef SEL_MINB
 #define SEL_MINB 4  // 64 registers (some spills) but 32 warps per SM: measured faster than 2
 #endif
-__global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
+__global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArgs a) {
 #ifdef CKV_SELPROF
   unsigned long long t_prev = gtimer();
 #endif
@@ -406,20 +406,20 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     prefetch_l2(st.split_state + (size_t)u * st.n_splits * H * CKV_SPLIT_FLOATS,
                 (uint32_t)((nb + st.blocks_per_split - 1) / st.blocks_per_split) * H * CKV_SPLIT_FLOATS * 4u);
   }
-  // ---- this thread's blocks tid + SEL_THREADS * j (j < KPT): order keys of l'_b in
+  // ---- this thread's blocks tid + NT * j (j < KPT): order keys of l'_b in
   // registers; strided ownership keeps every load coalesced
-#define BJ(j) (tid + SEL_THREADS * (j))
+#define BJ(j) (tid + NT * (j))
   uint32_t kk[KPT];
 #pragma unroll
   for (int j = 0; j < KPT; ++j) kk[j] = (BJ(j) < nb) ? okey(__ldg(lm + BJ(j))) : 0u;
 
   if (tid < D) S.qv[tid] = (float)(st.q[hu * D + tid] * 0.08838834764831845);
-  for (int i = tid; i < (c.max_blocks + 31) / 32; i += SEL_THREADS) fmask[i] = 0u;
+  for (int i = tid; i < (c.max_blocks + 31) / 32; i += NT) fmask[i] = 0u;
   __syncthreads();
 
   SELPROF(1);
   // ---- partial block on originals (attention.py:98-104) ------------------------
-  for (int t = warp; t < pl; t += SEL_THREADS / 32) {
+  for (int t = warp; t < pl; t += NT / 32) {
     const uint16_t* pk = c.partial_k + ((size_t)u * B + t) * D;
     float acc = 0.f;
 #pragma unroll
@@ -447,14 +447,14 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   {
     const float* spb = st.split_state + (((size_t)u * st.n_splits) * H + h) * CKV_SPLIT_FLOATS;
     float mloc = ninf(), dloc = 0.f;
-    for (int s2 = tid; s2 < nsp; s2 += SEL_THREADS) {
+    for (int s2 = tid; s2 < nsp; s2 += NT) {
       const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
       mloc = fmaxf(mloc, sp[0]);
       dloc = fmaxf(dloc, sp[2]);
     }
     const float M = block_max_f(mloc, S.redf);
     const float dm = block_max_f(dloc, S.redf);
-    for (int s2 = tid; s2 < nsp; s2 += SEL_THREADS) {
+    for (int s2 = tid; s2 < nsp; s2 += NT) {
       const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
       S.cum[s2] = (sp[0] == ninf()) ? 0.0 : (double)expf(sp[0] - M);
     }
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int w = 0; w < SEL_THREADS / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
       kmn = min(kmn, (uint32_t)S.wsum[w]);
       kmx = max(kmx, (uint32_t)S.wsum2[w]);
     }
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     for (int top = nbits; top > 0 && exact;) {
       const int shift = max(top - 11, 0);
       const int nbins = 1 << (top - shift);
-      for (int i = tid; i < 2048; i += SEL_THREADS) S.hist[i] = 0;
+      for (int i = tid; i < 2048; i += NT) S.hist[i] = 0;
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
       }
       __syncthreads();
       // suffix counts from the top bin down: thread t owns bins [hi-per, hi)
-      const int per = (nbins + SEL_THREADS - 1) / SEL_THREADS;
+      const int per = (nbins + NT - 1) / NT;
       const int hi_bin = nbins - tid * per;
       int loc = 0;
       for (int i = 1; i <= per; ++i)
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
     // rank sort (composite keys are distinct): position = #greater; the
     // candidate list is read as broadcast 16-byte pairs (a thread per candidate
     // measured faster than warp-cooperative variants)
-    for (int i = tid; i < n_sorted; i += SEL_THREADS) {
+    for (int i = tid; i < n_sorted; i += NT) {
       const unsigned long long x = S.cand[i];
       int r = 0;
       const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(S.cand);
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
 
   SELPROF(5);
   // ---- coverage K, clamp, rung 1 (attention.py:180-203, fallback.py:134-138) --------
-  for (int i = tid; i < n_sorted; i += SEL_THREADS) {
+  for (int i = tid; i < n_sorted; i += NT) {
     S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
   }
   __syncthreads();
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   }
   if (tid == 0) S.misc[4] = -1;
   __syncthreads();
-  for (int i = tid; i < n_sorted; i += SEL_THREADS)
+  for (int i = tid; i < n_sorted; i += NT)
     if (S.cum[i] >= pol.tau_cov && (i == 0 || S.cum[i - 1] < pol.tau_cov)) S.misc[4] = i + 1;
   __syncthreads();
   if (tid == 0) {
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(SEL_THREADS, SEL_MINB) k_select(StepArgs a) {
   __syncthreads();
   const int kcov = S.misc[4], kstar = S.misc[5], kp = S.misc[6];
   int32_t* order = st.order + hu * st.kcap;
-  for (int i = tid; i < kp; i += SEL_THREADS) {
+  for (int i = tid; i < kp; i += NT) {
     const int b = (int)(0xffffffffu - (uint32_t)(S.sortk[i] & 0xffffffffull));
     order[i] = b;
     atomicOr(&fmask[b >> 5], 1u << (b & 31));
@@ -922,16 +922,21 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   StepArgs a{*c, *st, *pol, PageView{}, u0};
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
-  if (nbh <= SEL_THREADS * 8)
-    k_select<8><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+  // few (unit, head) CTAs (e.g. 8-way KV-head sharding): 1024 threads per head, so
+  // each CTA's serial phases are shorter; otherwise 256 threads, 4 CTAs per SM
+  const bool wide = (long long)nu * st->n_heads <= 2 * 148 && nbh <= 1024 * 8;
+  if (wide)
+    k_select<8, 1024><<<dim3(st->n_heads, nu), 1024, smS, s>>>(a);
+  else if (nbh <= SEL_THREADS * 8)
+    k_select<8, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 16)
-    k_select<16><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+    k_select<16, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 32)
-    k_select<32><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+    k_select<32, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 64)
-    k_select<64><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+    k_select<64, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   else
-    k_select<128><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+    k_select<128, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -985,11 +990,12 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   static bool attrs = false;
   if (!attrs) {
     cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
-    cudaFuncSetAttribute(k_select<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<8, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<16, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<32, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<64, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_select<128, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
   const int U = c->n_units;
