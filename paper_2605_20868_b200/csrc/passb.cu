@@ -447,21 +447,35 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   }
   float canary = 0.f;
   double eF = 0.0, sF = 0.0;
-#pragma unroll 4
+#pragma unroll 8
   for (int k = 0; k < C; ++k) {
     const float* cs = chunk(k);
     const float sc = csc[k];
     den += cs[1] * sc;
     num += cs[8 + tid] * sc;
   }
-  if (tid == 0) {
-    for (int k = 0; k < C; ++k) {
+  {  // canary max and the F parts of E_val: chunks spread over the threads
+    __shared__ float cw[4];
+    __shared__ double ew[4], sw[4];
+    for (int k = tid; k < C; k += blockDim.x) {
       if (cm[k] == ninf()) continue;
       const float* cs = chunk(k);
       canary = fmaxf(canary, cs[2]);
       eF += reinterpret_cast<const double*>(cs + 4)[0];
       sF += reinterpret_cast<const double*>(cs + 4)[1];
     }
+    canary = warp_max(canary);
+    eF = warp_sum_d(eF);
+    sF = warp_sum_d(sF);
+    if ((tid & 31) == 0) {
+      cw[tid >> 5] = canary;
+      ew[tid >> 5] = eF;
+      sw[tid >> 5] = sF;
+    }
+    __syncthreads();
+    canary = fmaxf(fmaxf(cw[0], cw[1]), fmaxf(cw[2], cw[3]));
+    eF = (ew[0] + ew[1]) + (ew[2] + ew[3]);
+    sF = (sw[0] + sw[1]) + (sw[2] + sw[3]);
   }
   if (pl > 0) {
     const float sc = expf(hs.mp - M);
