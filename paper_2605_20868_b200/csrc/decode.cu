@@ -946,8 +946,23 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   }
   PageView pv{};
   if (sc) {
-    e = launch_scratch(c, st, sc, u0, nu, s);  // LRU accounting (+ side-stream page-in into slots)
-    if (e != cudaSuccess) return e;
+    // a scratch that holds every block and has no HBM slots needs no separate
+    // LRU pass: pass B decides hit / miss per union item (same counts as k_lru_fast)
+    const bool fuse = lru_ring(c->max_blocks, sc->key_capacity) == 0 &&
+                      lru_ring(c->max_blocks, sc->value_capacity) == 0 && sc->key_capacity > 0 &&
+                      sc->value_capacity > 0 && !sc->key_slots && !sc->value_slots &&
+                      !getenv("CKV_SEPARATE_LRU");
+    if (fuse) {
+      cudaMemsetAsync(st->page_stats + (size_t)u0 * 4, 0, sizeof(int32_t) * 4 * nu, s);
+      pv.fused = 1;
+      pv.klru = sc->key_lru;
+      pv.vlru = sc->value_lru;
+      pv.counters = sc->counters;
+      pv.page_stats = st->page_stats;
+    } else {
+      e = launch_scratch(c, st, sc, u0, nu, s);  // LRU accounting (+ side-stream page-in into slots)
+      if (e != cudaSuccess) return e;
+    }
     pv.kslots = sc->key_slots;
     pv.vslots = sc->value_slots;
     pv.kcap = sc->key_capacity;

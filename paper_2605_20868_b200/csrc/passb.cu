@@ -173,6 +173,17 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     fence_proxy_async();
     issue(mc, kb & 1);
   }
+  // fused LRU accounting (lane 0): hits / misses of this warp's items; the
+  // stamp exchange of item k is folded in at item k+1 (its latency off the path)
+  int lk_h = 0, lk_m = 0, lv_h = 0, lv_m = 0, req_k = 0, req_v = 0;
+  int pend_k = 1, pend_v = 1, pend_nk = 0, pend_nv = 0;
+  auto fold_lru = [&]() {
+    lk_m += (pend_nk > 0 && pend_k == 0);
+    lk_h += pend_nk - (pend_nk > 0 && pend_k == 0);
+    lv_m += (pend_nv > 0 && pend_v == 0);
+    lv_h += pend_nv - (pend_nv > 0 && pend_v == 0);
+    pend_nk = pend_nv = 0;
+  };
   int k = 0;
   for (; cur >= 0; ++k) {
     const int stg = (kb + k) & 1;
@@ -188,6 +199,15 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const uint32_t fm = ((uint32_t)e >> 24) & 0xfu, vm = ((uint32_t)e >> 28) & 0xfu;
     const bool inF = (fm >> h) & 1u, inV = (vm >> h) & 1u;
     if ((fm | vm) && lane == 0 && !mc.valid) atomicOr(&c.status[CKV_ST_TIER2], 1);
+    if (pv.fused && lane == 0) {
+      fold_lru();
+      pend_nk = __popc(fm);
+      pend_nv = __popc(vm);
+      req_k += pend_nk;
+      req_v += pend_nv;
+      if (pend_nk) pend_k = atomicExch(pv.klru + (size_t)u * pv.kstride + 4 + b, 1);
+      if (pend_nv) pend_v = atomicExch(pv.vlru + (size_t)u * pv.vstride + 4 + b, 1);
+    }
     const float smax = mc.smax;
     const float eta_b = mc.eta;
     mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
@@ -310,6 +330,26 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     e2 = e3;
   }
   kb += k;
+  if (pv.fused && lane == 0) {
+    fold_lru();
+    if (lk_h | lk_m | lv_h | lv_m) {
+      atomicAdd(pv.page_stats + u * 4 + 0, lk_h);
+      atomicAdd(pv.page_stats + u * 4 + 1, lk_m);
+      atomicAdd(pv.page_stats + u * 4 + 2, lv_h);
+      atomicAdd(pv.page_stats + u * 4 + 3, lv_m);
+      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(pv.counters + (size_t)u * 6);
+      atomicAdd(ctr + 0, (unsigned long long)lk_h);
+      atomicAdd(ctr + 1, (unsigned long long)lk_m);
+      atomicAdd(ctr + 2, (unsigned long long)lk_m * (B * D * 2));
+      atomicAdd(ctr + 3, (unsigned long long)lv_h);
+      atomicAdd(ctr + 4, (unsigned long long)lv_m);
+      atomicAdd(ctr + 5, (unsigned long long)lv_m * (B * D * 2));
+      atomicAdd(pv.klru + (size_t)u * pv.kstride + 0, req_k);  // clock T
+      atomicAdd(pv.klru + (size_t)u * pv.kstride + 2, lk_m);   // resident count
+      atomicAdd(pv.vlru + (size_t)u * pv.vstride + 0, req_v);
+      atomicAdd(pv.vlru + (size_t)u * pv.vstride + 2, lv_m);
+    }
+  }
 
   // ---- reduce within the warp (per head), then across the 4 warps ----------
   dden += __shfl_xor_sync(0xffffffffu, dden, 4);

@@ -33,6 +33,13 @@ struct PageView {
   const int32_t* kslot_of;  // per unit: + u * kstride
   const int32_t* vslot_of;
   int32_t kstride, vstride, kcap, vcap;
+  // fused LRU accounting (no-eviction scratch without HBM slots): pass B stamps
+  // the requested blocks and counts hits / misses itself
+  int32_t* klru;
+  int32_t* vlru;
+  int64_t* counters;
+  int32_t* page_stats;
+  int32_t fused;
 };
 
 struct StepArgs {
