@@ -119,9 +119,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
   const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
   // Per-item metadata is software-pipelined so no dependent global load sits
-  // on the critical path: work entries are read three items ahead, the slot /
-  // key-scale / eta / Tier-2-valid words of an item one iteration before its
-  // TMA is issued (the item after that) and consumed.
+  // on the critical path: work entries are read four items ahead, the slot /
+  // key-scale / eta / Tier-2-valid / stash words of an item two iterations before
+  // its TMA is issued and three before it is consumed.
   struct Meta {
     int e, sl, valid, st;
     float smax, eta;
@@ -166,9 +166,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   int cur = item_at(0);
   int i1 = item_at(1);
   int i2 = item_at(2);
+  int i3 = item_at(3);
   Meta mc = load_meta(cur >= 0 ? work[cur] : 0, cur >= 0);
   Meta mn = load_meta(i1 >= 0 ? work[i1] : 0, i1 >= 0);
-  int e2 = (i2 >= 0) ? work[i2] : 0;  // work entry of item k+2 (read one iteration ahead)
+  Meta mnn = load_meta(i2 >= 0 ? work[i2] : 0, i2 >= 0);
+  int e3 = (i3 >= 0) ? work[i3] : 0;  // work entry of item k+3 (read one iteration ahead)
   if (lane == 0 && cur >= 0) {
     fence_proxy_async();
     issue(mc, kb & 1);
@@ -188,8 +190,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   for (; cur >= 0; ++k) {
     const int stg = (kb + k) & 1;
     const int nxt = i1;
-    const int i3 = item_at(k + 3);
-    const int e3 = (i3 >= 0) ? work[i3] : 0;  // consumed in the next iteration
+    const int i4 = item_at(k + 4);
+    const int e4 = (i4 >= 0) ? work[i4] : 0;  // consumed in the next iteration
     if (lane == 0 && nxt >= 0) {
       fence_proxy_async();
       issue(mn, stg ^ 1);
@@ -325,9 +327,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     cur = nxt;
     i1 = i2;
     mc = mn;
-    mn = load_meta(e2, i2 >= 0);
+    mn = mnn;
+    mnn = load_meta(e3, i3 >= 0);  // a full iteration before its TMA is issued
     i2 = i3;
-    e2 = e3;
+    i3 = i4;
+    e3 = e4;
   }
   kb += k;
   if (pv.fused && lane == 0) {
