@@ -65,14 +65,12 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
                                                     int lane) {
   const float* sig = reinterpret_cast<const float*>(rec + OFF_KSCALE);
   const float* zz = reinterpret_cast<const float*>(rec + OFF_KOFF);
-  const bool odd = (lane >> 2) & 1;
   const int es = ilogbf(smax) + 1;    // smax < 2^es
   // fma(qsc, sigma, 1.5*2^(23+es)) has the same mantissa bits as
   // fma(qsc, sigma*2^-es, 1.5*2^23) (exact power-of-two scaling): the bytes of
   // U = X + 2^22 come out unchanged, except that byte 2 carries the exponent
   // LSB (es & 1) in its top bit, removed below with the sum-of-codes column.
   const float magic_b = __uint_as_float(((uint32_t)(150 + es) << 23) | 0x400000u);
-  const uint32_t sel0 = ((lane >> 2) & 1) ? 0x5151u : 0x4040u;  // byte 1 or 0 of y0,y1
   // Lanes l and l^4 (byte parity of the same head) share their y values: each
   // computes 4 of the 8 channels of a k-tile (one 16-byte sigma / z load each
   // instead of two) and they swap halves with a shuffle.  The shared-memory
@@ -88,7 +86,7 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
     const float4 z4 = *reinterpret_cast<const float4*>(zz + cm);
     const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
     const float zv[4] = {z4.x, z4.y, z4.z, z4.w};
-    uint32_t ym[4], yo[4];
+    uint32_t ym[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const float q = f.qsc[kt * 4 + i];
@@ -96,19 +94,19 @@ __device__ __forceinline__ BlockScores phase1_block(const QFrag& f, const uint8_
       dacc = fmaf(fabsf(q), sv[i], dacc);
       zacc = fmaf(q, zv[i], zacc);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) yo[i] = __shfl_xor_sync(0xffffffffu, ym[i], 4);
-    // byte planes of my half (m) and the partner's half (o)
-    const uint32_t pm0 = __byte_perm(__byte_perm(ym[0], ym[1], sel0), __byte_perm(ym[2], ym[3], sel0), 0x5410);
-    const uint32_t po0 = __byte_perm(__byte_perm(yo[0], yo[1], sel0), __byte_perm(yo[2], yo[3], sel0), 0x5410);
-    const uint32_t pm2 = __byte_perm(__byte_perm(ym[0], ym[1], 0x6262u), __byte_perm(ym[2], ym[3], 0x6262u), 0x5410);
-    const uint32_t po2 = __byte_perm(__byte_perm(yo[0], yo[1], 0x6262u), __byte_perm(yo[2], yo[3], 0x6262u), 0x5410);
-    const uint32_t b00 = half ? po0 : pm0, b01 = half ? pm0 : po0;
-    uint32_t b10 = half ? po2 : pm2, b11 = half ? pm2 : po2;
-    if (odd) {
-      b10 = 0x01010101u;
-      b11 = 0x01010101u;
-    }
+    // all three byte planes of my 4 y values (7 PRMT), then one shuffle of the
+    // plane the partner needs for tile 0 (its byte parity) and one of byte 2
+    const uint32_t a01 = __byte_perm(ym[0], ym[1], 0x5140u), a23 = __byte_perm(ym[2], ym[3], 0x5140u);
+    const uint32_t c01 = __byte_perm(ym[0], ym[1], 0x6262u), c23 = __byte_perm(ym[2], ym[3], 0x6262u);
+    const uint32_t pl0 = __byte_perm(a01, a23, 0x5410u);  // byte 0 of y0..y3
+    const uint32_t pl1 = __byte_perm(a01, a23, 0x7632u);  // byte 1
+    const uint32_t pl2 = __byte_perm(c01, c23, 0x5410u);  // byte 2
+    const uint32_t r1 = __shfl_xor_sync(0xffffffffu, half ? pl0 : pl1, 4);  // partner's byte p
+    const uint32_t r2 = __shfl_xor_sync(0xffffffffu, pl2, 4);               // partner's byte 2
+    // tile 0: byte p of channels cb..cb+3 (b00) and cb+16..cb+19 (b01);
+    // tile 1: byte 2 (even lane/4) or the ones column (odd lane/4)
+    const uint32_t b00 = half ? r1 : pl0, b01 = half ? pl1 : r1;
+    const uint32_t b10 = half ? 0x01010101u : pl2, b11 = half ? 0x01010101u : r2;
     const uint4 a = *reinterpret_cast<const uint4*>(rec + OFF_KCODES + kt * 512 + lane * 16);
     mma_s8u8(d0, a, b00, b01);
     mma_s8u8(d1, a, b10, b11);
