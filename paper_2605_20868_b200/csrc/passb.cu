@@ -118,31 +118,48 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const PageView& pv = a.pv;
   const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
   const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
-  // Per-item metadata is software-pipelined so no dependent global load sits
-  // on the critical path: work entries are read four items ahead, the slot /
-  // key-scale / eta / Tier-2-valid / stash words of an item two iterations before
-  // its TMA is issued and three before it is consumed.
+  // Per-item metadata (work entry, slot, key-scale max, eta, Tier-2 valid,
+  // stash epoch) is gathered lane-parallel: lane l holds item j = 32 w + l of
+  // the warp's sequence in set w & 1; the set of window w + 2 is refilled at
+  // the start of window w + 1 (work entries) and 8 items later (the dependent
+  // words), so no load latency sits on the item loop.  Items are fetched from
+  // their lane with shuffles two iterations before their copies are issued.
   struct Meta {
     int e, sl, valid, st;
     float smax, eta;
   };
   const float* stash_u = st.stash ? st.stash + (size_t)u * c.max_blocks * 64 : nullptr;
-  auto load_meta = [&](int e2, bool ok) -> Meta {  // work entries may have bit 31 set
-    Meta m;
-    m.e = e2;
+  int le[2], lsl[2], lval[2], lsep[2];
+  float lsm[2], let_[2];
+  auto load_e = [&](int s, int kbase) {
+    const int it = item_at(kbase + lane);
+    const int e2 = (it >= 0) ? work[it] : -1;
+    if (s) le[1] = e2; else le[0] = e2;
+  };
+  auto load_words = [&](int s) {
+    const int e2 = s ? le[1] : le[0];
+    const bool ok = e2 != -1;
     const int b2 = e2 & 0xffffff;
-    m.sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
-    m.smax = ok ? c.kscale_max[ubk + b2] : 1.f;
-    m.eta = ok ? eta[b2] : 0.f;
-    m.valid = ok ? c.tier2_valid[ubk + b2] : 1;
+    const int sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
+    const float sm = ok ? c.kscale_max[ubk + b2] : 1.f;
+    const float et = ok ? eta[b2] : 0.f;
+    const int va = ok ? c.tier2_valid[ubk + b2] : 1;
+    const int se = (ok && stash_u) ? st.stash_epoch[ubk + b2] : 0;
+    if (s) { lsl[1] = sl; lsm[1] = sm; let_[1] = et; lval[1] = va; lsep[1] = se; }
+    else   { lsl[0] = sl; lsm[0] = sm; let_[0] = et; lval[0] = va; lsep[0] = se; }
+  };
+  auto fetch = [&](int j) -> Meta {  // warp-uniform j
+    const int s = (j >> 5) & 1, src = j & 31;
+    Meta m;
+    m.e = __shfl_sync(0xffffffffu, s ? le[1] : le[0], src);
+    m.sl = __shfl_sync(0xffffffffu, s ? lsl[1] : lsl[0], src);
+    m.smax = __shfl_sync(0xffffffffu, s ? lsm[1] : lsm[0], src);
+    m.eta = __shfl_sync(0xffffffffu, s ? let_[1] : let_[0], src);
+    m.valid = __shfl_sync(0xffffffffu, s ? lval[1] : lval[0], src);
+    const int se = __shfl_sync(0xffffffffu, s ? lsep[1] : lsep[0], src);
     // usable when this step's pass A stashed every head the item is promoted for
-    if (ok && stash_u) {
-      const int se = st.stash_epoch[ubk + b2];
-      const uint32_t need = (((uint32_t)e2 >> 24) | ((uint32_t)e2 >> 28)) & 0xfu;
-      m.st = ((se >> 4) == st.epoch) && ((need & ~(uint32_t)se) == 0u);
-    } else {
-      m.st = 0;
-    }
+    const uint32_t need = (((uint32_t)m.e >> 24) | ((uint32_t)m.e >> 28)) & 0xfu;
+    m.st = stash_u && m.e != -1 && ((se >> 4) == st.epoch) && ((need & ~(uint32_t)se) == 0u);
     return m;
   };
   auto issue = [&](const Meta& m, int stg) {
@@ -163,14 +180,14 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       bulk_g2s(S.kt[warp][stg], src, B * D * 2, &S.bar[warp][stg]);
     }
   };
+  load_e(0, 0);
+  load_e(1, 32);
+  load_words(0);
+  load_words(1);
   int cur = item_at(0);
   int i1 = item_at(1);
-  int i2 = item_at(2);
-  int i3 = item_at(3);
-  Meta mc = load_meta(cur >= 0 ? work[cur] : 0, cur >= 0);
-  Meta mn = load_meta(i1 >= 0 ? work[i1] : 0, i1 >= 0);
-  Meta mnn = load_meta(i2 >= 0 ? work[i2] : 0, i2 >= 0);
-  int e3 = (i3 >= 0) ? work[i3] : 0;  // work entry of item k+3 (read one iteration ahead)
+  Meta mc = fetch(0);
+  Meta mn = fetch(1);
   if (lane == 0 && cur >= 0) {
     fence_proxy_async();
     issue(mc, kb & 1);
@@ -190,8 +207,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   for (; cur >= 0; ++k) {
     const int stg = (kb + k) & 1;
     const int nxt = i1;
-    const int i4 = item_at(k + 4);
-    const int e4 = (i4 >= 0) ? work[i4] : 0;  // consumed in the next iteration
+    if ((k & 31) == 0 && k >= 32) load_e(((k >> 5) + 1) & 1, k + 32);
+    if ((k & 31) == 8 && k >= 32) load_words(((k >> 5) + 1) & 1);
     if (lane == 0 && nxt >= 0) {
       fence_proxy_async();
       issue(mn, stg ^ 1);
@@ -325,13 +342,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     }
     __syncwarp();
     cur = nxt;
-    i1 = i2;
+    i1 = item_at(k + 2);
     mc = mn;
-    mn = mnn;
-    mnn = load_meta(e3, i3 >= 0);  // a full iteration before its TMA is issued
-    i2 = i3;
-    i3 = i4;
-    e3 = e4;
+    mn = fetch(k + 2);
   }
   kb += k;
   if (pv.fused && lane == 0) {
