@@ -224,8 +224,10 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     pv_frag(F, *reinterpret_cast<const float4*>(&S.pbuf[warp][hb][4 * (lane & 3)]), lo_lane);
     pv_block_sub(acc, accz, F, rec, lane);
     __syncwarp();
+    // refill the stage: it is only ever read by this warp's generic loads (all
+    // consumed before the __syncwarp above) and written by the bulk copy, so no
+    // proxy fence is needed (write-after-read, no generic writes to order)
     if (lane == 0 && i + PA_STAGES < nmine) {
-      fence_proxy_async();
       mbar_expect_tx(&S.bar[warp][s], REC);
       bulk_g2s(S.stage[warp][s], ubase + (size_t)(b + PA_WARPS * PA_STAGES) * REC, REC,
                &S.bar[warp][s]);
