@@ -396,19 +396,61 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        kd = torch.empty((U, 1, 128), dtype=torch.float16, device=dev)
-        vd = torch.empty_like(kd)
+        serial = os.environ.get("CKV_E2E_SERIAL") == "1"
+        comp = torch.cuda.current_stream(dev)
+        cs = torch.cuda.Stream(device=dev)  # copy stream: PCIe transfers beside the kernels
+        # double-buffered device staging: step i+1's inputs land while step i runs,
+        # step i's output leaves while step i+1 runs
+        qd = [torch.empty_like(dec.q) for _ in range(2)]
+        kd = [torch.empty((U, 1, 128), dtype=torch.float16, device=dev) for _ in range(2)]
+        vd = [torch.empty_like(kd[0]) for _ in range(2)]
+        od = [torch.empty_like(dec.out) for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_used = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        ev_d2h = [torch.cuda.Event() for _ in range(2)]
+
+        def stage_in(i):  # H2D of step i's queries and new token on the copy stream
+            j, b = i % NP, i % 2
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_used[b])  # step i-2 is done with these buffers
+                qd[b].copy_(qh[j], non_blocking=True)
+                kd[b].copy_(kh[j], non_blocking=True)
+                vd[b].copy_(vh[j], non_blocking=True)
+                ev_in[b].record(cs)
+
+        for ev in ev_used + ev_d2h:
+            ev.record(comp)
+        torch.cuda.synchronize()
         e0 = time.perf_counter()
         prev = None
+        if not serial:
+            stage_in(0)
         for i in range(E):
-            j = i % NP
-            dec.q.copy_(qh[j], non_blocking=True)            # H2D: this step's queries
-            p = dec.step_async(None, reduce_flags)          # + D2H of the certificates
-            exchange()
-            oh.copy_(dec.out, non_blocking=True)             # D2H: the attention outputs
-            kd.copy_(kh[j], non_blocking=True)               # H2D: the step's new token
-            vd.copy_(vh[j], non_blocking=True)
-            cache.append(kd, vd, validate="defer")
+            j, b = i % NP, i % 2
+            if serial:
+                dec.q.copy_(qh[j], non_blocking=True)            # H2D: this step's queries
+                p = dec.step_async(None, reduce_flags)          # + D2H of the certificates
+                exchange()
+                oh.copy_(dec.out, non_blocking=True)             # D2H: the attention outputs
+                kd[0].copy_(kh[j], non_blocking=True)            # H2D: the step's new token
+                vd[0].copy_(vh[j], non_blocking=True)
+                cache.append(kd[0], vd[0], validate="defer")
+            else:
+                if i + 1 < E:
+                    stage_in(i + 1)
+                comp.wait_event(ev_in[b])
+                p = dec.step_async(qd[b], reduce_flags)         # + D2H of the certificates
+                exchange()
+                comp.wait_event(ev_d2h[b])                      # step i-2's output has left od[b]
+                od[b].copy_(dec.out, non_blocking=True)
+                ev_out[b].record(comp)
+                cache.append(kd[b], vd[b], validate="defer")
+                ev_used[b].record(comp)
+                with torch.cuda.stream(cs):                     # D2H: the attention outputs
+                    cs.wait_event(ev_out[b])
+                    oh.copy_(od[b], non_blocking=True)
+                    ev_d2h[b].record(cs)
             if prev is not None:
                 prev.result()  # host reads step i-1's bound report while step i runs
             prev = p
