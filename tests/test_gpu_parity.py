@@ -455,3 +455,48 @@ def test_step_async_matches_step_and_defers_append_check(ck):
     ca.append(k[:, :1], v[:, :1], validate="defer")  # the cache keeps working
     da.step_async(qs[1]).result()
     assert ca.num_tokens == t0 + 1
+
+
+@pytest.mark.parametrize("env", [{"CKV_NO_STASH": "1"}, {"CKV_CHUNKS": "2"}, {"CKV_SEPARATE_LRU": "1"},
+                                 {"CKV_SEPARATE_UNION": "1"}],
+                         ids=["no_stash", "chunks2", "separate_lru", "separate_union"])
+def test_alternate_paths_bit_identical(ck, monkeypatch, env):
+    """The A/B knobs switch between code paths that compute the same values: the
+    phase-1 score stash (pass A's scores reused by pass B), unit-chunked overlap of
+    the tail kernels, the fused vs separate LRU scratch accounting and the union
+    list built by the last selection CTA vs its own launch.  Outputs,
+    certificates and page statistics must be bit-identical to the default path."""
+    rng = np.random.default_rng(33)
+    U, n = 20, 3000
+    k = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    v = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    qs = [torch.from_numpy(rng.standard_normal((U, 4, 128))).cuda() for _ in range(4)]
+    kn = torch.from_numpy(rng.standard_normal((4, U, 1, 128))).half().cuda()
+    pol = ck.PolicyConfig(exploration_rate=0.0, k_max=24)
+
+    def run():
+        cache = ck.DeviceKVCache(U, n + 16)
+        cache.append(k, v)
+        dec = ck.CertifiedDecoder(cache, pol, n_heads=4, scratch=ck.ScratchCache(cache.max_blocks))
+        outs, certs, pages = [], [], []
+        stashed = 0
+        for i, q in enumerate(qs):
+            r = dec.step(q)
+            if getattr(dec, "stash_epoch", None) is not None:
+                stashed += int(((dec.stash_epoch >> 4) == dec.st.epoch).sum())
+            outs.append(dec.out.cpu().numpy().copy())
+            certs.append(np.array(r.cert, copy=True))
+            pages.append(None if r.page_stats is None else np.array(r.page_stats, copy=True))
+            cache.append(kn[i], kn[i])
+        return outs, certs, pages, stashed
+
+    base = run()
+    assert base[3] > 0  # the default path did use the stash
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    alt = run()
+    for s in range(len(qs)):
+        np.testing.assert_array_equal(alt[0][s], base[0][s], err_msg=f"output step {s}")
+        np.testing.assert_array_equal(alt[1][s], base[1][s], err_msg=f"certificates step {s}")
+        if base[2][s] is not None:
+            np.testing.assert_array_equal(alt[2][s], base[2][s], err_msg=f"page stats step {s}")
