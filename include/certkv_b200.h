@@ -234,15 +234,18 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
  *                      across ranks here (harness.py:362-372 per layer).
  *   ckv_decode_finish: every head of a flagged group returns dense
  *                      (dense_all_heads); exact dense fallback of rung-3/4 heads.
+ *                      With a scratch that has HBM slots (Tier-2 in host RAM), blocks
+ *                      resident in a slot are read from HBM, the rest from Tier-2
+ *                      (same bytes either way; NULL scratch: Tier-2 only).
  *   ckv_decode_end = ckv_decode_flags + ckv_decode_finish. */
 ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                             const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
 ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                             int32_t host_max_blocks, void* stream);
-ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, int32_t host_max_blocks,
-                             void* stream);
+ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, const ckv_scratch* scratch,
+                             int32_t host_max_blocks, void* stream);
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                          int32_t host_max_blocks, void* stream);
+                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream);
 
 /* Unpack Tier-1 for parity: codes i8 [nb][16][128], kscale/koffset f32 [nb][128],
  * vcodes u8 [nb][16][128], vscale/voffset fp16 [nb][16][8], for blocks

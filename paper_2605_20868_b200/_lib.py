@@ -101,10 +101,11 @@ def load():
         "ckv_decode_begin": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
                                    ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_decode_end": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
-                                 ctypes.POINTER(CkvStep), I32, P]),
+                                 ctypes.POINTER(CkvStep), ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_decode_flags": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvPolicy),
                                    ctypes.POINTER(CkvStep), I32, P]),
-        "ckv_decode_finish": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvStep), I32, P]),
+        "ckv_decode_finish": (I32, [ctypes.POINTER(CkvCache), ctypes.POINTER(CkvStep),
+                                    ctypes.POINTER(CkvScratch), I32, P]),
         "ckv_read_tier1": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, P, P, P, P, P, P, P]),
         "ckv_fault_offset": (I32, [ctypes.POINTER(CkvCache), I32, I32, I32, ctypes.c_float, P]),
         "ckv_tier2_drop": (I32, [ctypes.POINTER(CkvCache), I32, I32, P]),

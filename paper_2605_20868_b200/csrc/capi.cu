@@ -13,7 +13,7 @@ cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
 cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, const ckv_scratch*, int,
                           cudaStream_t);
-cudaError_t launch_dense(const ckv_cache*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_dense(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, cudaStream_t);
 cudaError_t launch_group_flags(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
@@ -136,19 +136,19 @@ ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step*
   return st_of(ckv::launch_group_flags(c, st, S(stream)));
 }
 
-ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, int32_t host_max_blocks,
-                             void* stream) {
+ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, const ckv_scratch* scratch,
+                             int32_t host_max_blocks, void* stream) {
   ckv_policy dummy{};
   dummy.k_max = 1;
   if (!step_ok(c, &dummy, st, host_max_blocks)) return CKV_EINVAL;
-  return st_of(ckv::launch_dense(c, st, (host_max_blocks + 1) * CKV_BLOCK, S(stream)));
+  return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, S(stream)));
 }
 
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                          int32_t host_max_blocks, void* stream) {
+                          const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
   ckv_status r = ckv_decode_flags(c, pol, st, host_max_blocks, stream);
   if (r != CKV_OK) return r;
-  return ckv_decode_finish(c, st, host_max_blocks, stream);
+  return ckv_decode_finish(c, st, scratch, host_max_blocks, stream);
 }
 
 ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
@@ -157,7 +157,7 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
   if (r != CKV_OK) return r;
   int32_t* en = st->explore_n;
   st->explore_n = nullptr;  // samples need the begin half's K': use begin/end for exploration
-  r = ckv_decode_end(c, pol, st, host_max_blocks, stream);
+  r = ckv_decode_end(c, pol, st, scratch, host_max_blocks, stream);
   st->explore_n = en;
   return r;
 }

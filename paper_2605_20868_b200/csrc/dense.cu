@@ -25,6 +25,7 @@ struct DenseArgs {
   int32_t group;     // (unused)
   int32_t n_dsplit;  // splits per dense unit of this launch (set on device from the count)
   int32_t blk_per_split;  // (unused)
+  PageView pv;  // HBM scratch slots (Tier-2 in host RAM): resident blocks are read from HBM
 };
 
 __device__ __forceinline__ float dninf() { return __int_as_float(0xff800000); }
@@ -197,12 +198,25 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   float acc[NG][4];
 #pragma unroll
   for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+  // a block already paged into an HBM slot this or an earlier step (its bytes are
+  // the Tier-2 bytes) is read from the slot instead of over PCIe from host Tier-2
+  const PageView& pv = a.pv;
+  const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
+  const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
+  int ksl = (kslot && b0 + warp < b1) ? kslot[b0 + warp] : -1;
+  int vsl = (vslot && b0 + warp < b1) ? vslot[b0 + warp] : -1;
   for (int b = b0 + warp; b < b1; b += DN_WARPS) {
-    const uint4* vf = reinterpret_cast<const uint4*>(c.tier2_v + (ubk + b) * B * D);
+    const uint4* vf = reinterpret_cast<const uint4*>(
+        (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
+    const uint4* kf = reinterpret_cast<const uint4*>(
+        (ksl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + ksl) * B * D : c.tier2_k + (ubk + b) * B * D);
+    const int bn = b + DN_WARPS;  // the next block's slots, loaded one iteration ahead
+    ksl = (kslot && bn < b1) ? kslot[bn] : -1;
+    vsl = (vslot && bn < b1) ? vslot[bn] : -1;
     uint4 av[NG];
 #pragma unroll
     for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
-    const float2 s = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
+    const float2 s = orig_block(f16, kf, lane);
     float bmx = fmaxf(s.x, s.y);
     bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 4));
     bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
 extern int g_launches;
 
 cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStream_t s) {
-  DenseArgs a{*c, *st, 0, 0, 0};
+  DenseArgs a{*c, *st, 0, 0, 0, PageView{}};
   cudaMemsetAsync(st->group_flags, 0, sizeof(int32_t) * st->n_groups, s);
   const int n = c->n_units * st->n_heads;
   k_group_flags<<<(n + 255) / 256, 256, 0, s>>>(a);
@@ -276,9 +290,20 @@ cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, int host_max_tokens, cudaStream_t s) {
+cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc,
+                         int host_max_tokens, cudaStream_t s) {
   (void)host_max_tokens;
-  DenseArgs a{*c, *st, 0, 1, 0};
+  DenseArgs a{*c, *st, 0, 1, 0, PageView{}};
+  if (sc && (sc->key_slots || sc->value_slots)) {
+    a.pv.kslots = sc->key_capacity > 0 ? sc->key_slots : nullptr;
+    a.pv.vslots = sc->value_capacity > 0 ? sc->value_slots : nullptr;
+    a.pv.kcap = sc->key_capacity;
+    a.pv.vcap = sc->value_capacity;
+    a.pv.kstride = lru_words(c->max_blocks, sc->key_capacity);
+    a.pv.vstride = lru_words(c->max_blocks, sc->value_capacity);
+    a.pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
+    a.pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
+  }
   static int slots = 0;
   if (!slots) {
     int dev = 0, sms = 0, per = 0;

@@ -185,7 +185,7 @@ class CertifiedDecoder:
         _lib.check(self.lib.ckv_decode_flags(*args, nbk, stream), "ckv_decode_flags")
         reduce_flags(self.group_flags)
         _lib.check(self.lib.ckv_decode_finish(ctypes.byref(self.cache.c), ctypes.byref(self.st),
-                                              nbk, stream), "ckv_decode_finish")
+                                              sc, nbk, stream), "ckv_decode_finish")
 
     def step(self, queries, rng=None):
         """Certified attention for all units: queries [U, nh, 128] (float64).
@@ -294,8 +294,9 @@ class CertifiedDecoder:
         self.explore_n.copy_(self.explore_n_host, non_blocking=True)
         self.explore_pos.copy_(self.explore_pos_host, non_blocking=True)
         self.st.explore_n = _ptr(self.explore_n)
+        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
         code = self.lib.ckv_decode_end(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                       ctypes.byref(self.st), nbk, stream)
+                                       ctypes.byref(self.st), sc, nbk, stream)
         self.st.explore_n = None
         _lib.check(code, "ckv_decode_end")
         out = self._finish()

@@ -330,6 +330,38 @@ def test_host_tier2_matches_device_tier2(ck):
     assert outs[0][1] == outs[1][1]
 
 
+def test_dense_reads_hbm_slots_bit_identical(ck):
+    """Rung-3/4 dense units with Tier-2 in host RAM read their blocks already
+    paged into HBM slots from the slots and the rest from host Tier-2: outputs,
+    kinds and certificates equal those of the same steps with Tier-2 in HBM."""
+    U, N = 4, 4000
+    g = torch.Generator(device="cuda").manual_seed(12)
+    k = torch.randn((U, N, 128), generator=g, device="cuda", dtype=torch.float32)
+    v = torch.randn((U, N, 128), generator=g, device="cuda", dtype=torch.float32)
+    qs = [torch.randn((U, 4, 128), generator=g, device="cuda", dtype=torch.float64)
+          for _ in range(3)]
+    runs = []
+    for where in ("device", "host"):
+        cache = ck.DeviceKVCache(U, N + 8, tier2=where)
+        cache.append(k, v)
+        dec = ck.CertifiedDecoder(cache, ck.PolicyConfig(exploration_rate=0.0, v_tol=0.01),
+                                  n_heads=4, scratch=ck.ScratchCache(cache.max_blocks),
+                                  rung4_group=1)
+        res = []
+        for s, q in enumerate(qs):
+            if s == 1:
+                cache.corrupt_offset(1, 3, 0, 1e4)  # canary on unit 1 -> its group goes dense
+            r = dec.step(q)
+            res.append((r.out.clone(), r.kinds.copy(), r.cert.copy()))
+        runs.append(res)
+    for s, (a, b) in enumerate(zip(*runs)):
+        assert torch.equal(a[0], b[0]), s
+        assert np.array_equal(a[1], b[1]), s
+        assert a[2].tobytes() == b[2].tobytes(), s
+    assert runs[1][1][1][1].all() and runs[1][2][1][1].all()
+    assert not runs[1][0][1][1].any()
+
+
 @pytest.mark.parametrize("name", ["explore", "greedy"])
 def test_exploration_and_greedy_parity(ck, name, tmp_path):
     """Exploration spot checks (host Philox draws, device rescoring) and the greedy
