@@ -90,6 +90,11 @@ __host__ __device__ inline int lru_ring(int max_blocks, int cap) {
   return R;
 }
 __host__ __device__ inline int lru_words(int max_blocks, int cap) {
+  return 4 + 3 * max_blocks + lru_ring(max_blocks, cap);
+}
+// per-block epoch of the step that missed it into its slot (the slot is filled by
+// that step's pass B, or by k_pagein); = slot table + max_blocks
+__host__ __device__ inline int lru_fresh_offset(int max_blocks, int cap) {
   return 4 + 2 * max_blocks + lru_ring(max_blocks, cap);
 }
 // slot table (HBM slot of each resident block, -1 otherwise) inside an LRU state
@@ -160,6 +165,19 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
+}
+// shared -> global bulk copy (bulk async-group); wait_read: the source may be refilled
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -97,6 +97,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const float p2S = pow2f(Sx);
 
   const size_t ubk = (size_t)u * c.max_blocks;
+  const int maxb = c.max_blocks;
   const int32_t* work = st.work + (size_t)u * st.wcap;
   const float* eta = c.eta + ubk;
   float* lm2 = st.lm2 + ((size_t)u * nh + hq) * c.max_blocks;
@@ -140,7 +141,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const int e2 = s ? le[1] : le[0];
     const bool ok = e2 != -1;
     const int b2 = e2 & 0xffffff;
-    const int sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
+    int sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
+    // missed into its slot this step: read Tier-2, fill the slot (bit 30 of sl)
+    if (sl >= 0 && kslot[maxb + b2] == st.epoch) sl |= 0x40000000;
     const float sm = ok ? c.kscale_max[ubk + b2] : 1.f;
     const float et = ok ? eta[b2] : 0.f;
     const int va = ok ? c.tier2_valid[ubk + b2] : 1;
@@ -175,8 +178,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
     }
     if (keys) {
-      const uint16_t* src = (m.sl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
-                                        : c.tier2_k + (ubk + b2) * B * D;
+      const uint16_t* src = (m.sl >= 0 && !(m.sl & 0x40000000))
+                                ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
+                                : c.tier2_k + (ubk + b2) * B * D;
       bulk_g2s(S.kt[warp][stg], src, B * D * 2, &S.bar[warp][stg]);
     }
   };
@@ -186,6 +190,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   load_words(1);
   int cur = item_at(0);
   int i1 = item_at(1);
+  bool s2g_pending = false;  // lane 0: a slot fill (shared -> global) may be reading a stage
   Meta mc = fetch(0);
   Meta mn = fetch(1);
   if (lane == 0 && cur >= 0) {
@@ -210,6 +215,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     if ((k & 31) == 0 && k >= 32) load_e(((k >> 5) + 1) & 1, k + 32);
     if ((k & 31) == 8 && k >= 32) load_words(((k >> 5) + 1) & 1);
     if (lane == 0 && nxt >= 0) {
+      if (s2g_pending) bulk_wait_read();  // a slot fill may still read the stage
+      s2g_pending = false;
       fence_proxy_async();
       issue(mn, stg ^ 1);
     }
@@ -231,6 +238,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const float eta_b = mc.eta;
     mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
     const uint8_t* rec = S.rec[warp][stg];
+    if (fm && mc.sl >= 0 && (mc.sl & 0x40000000) && lane == 0) {  // page-in of a missed key tile
+      bulk_s2g(const_cast<uint16_t*>(pv.kslots) + ((size_t)u * pv.kcap + (mc.sl & 0x3fffffff)) * B * D,
+               S.kt[warp][stg], B * D * 2);
+      s2g_pending = true;
+    }
 
     BlockScores r;
     if (mc.st) {  // bit-identical to phase1_block in pass A (that is where they come from)
@@ -332,11 +344,17 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       split_h2(p4.z, p4.w, h23, l23);
       const uint32_t b0 = lo_lane ? l01 : h01, b1 = lo_lane ? l23 : h23;
       const int vsl = vslot ? vslot[b] : -1;
+      const bool vfill = vsl >= 0 && vslot[maxb + b] == st.epoch;  // missed this step
       const uint4* vf = reinterpret_cast<const uint4*>(
-          (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
+          (vsl >= 0 && !vfill) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
       uint4 av[NG];
 #pragma unroll
       for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
+      if (vfill) {  // page-in of a missed value tile
+        uint4* dst = reinterpret_cast<uint4*>(const_cast<uint16_t*>(pv.vslots) + ((size_t)u * pv.vcap + vsl) * B * D);
+#pragma unroll
+        for (int g = 0; g < NG; ++g) dst[g * 32 + lane] = av[g];
+      }
 #pragma unroll
       for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, b0, b1);
     }
@@ -347,6 +365,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     mn = fetch(k + 2);
   }
   kb += k;
+  if (lane == 0 && s2g_pending) bulk_wait_all();  // slot fills done before the stages are reused / exit
   if (pv.fused && lane == 0) {
     fold_lru();
     if (lk_h | lk_m | lv_h | lv_m) {

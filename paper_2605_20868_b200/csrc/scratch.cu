@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   const int cap = a.cap;
   long long hits = 0, misses = 0;
   int32_t* mlist = a.miss_list ? a.miss_list + ((size_t)u * 2 + a.kind) * a.miss_cap : nullptr;
+  int32_t* fresh_g = L + lru_fresh_offset(maxb, cap);
 
   for (int h = 0; h < st.n_heads; ++h) {
     const size_t hu = (size_t)u * st.n_heads + h;
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
         const int b = req[i];
         if (stamp[b] == 0) {
           slot[b] = count + r;
+          fresh_g[b] = st.epoch;
           if (mlist) {
             const int k = atomicAdd(&nmiss, 1);
             if (k < a.miss_cap) mlist[k] = b;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
               s = count++;
             }
             slot[b] = s;
+            fresh_g[b] = st.epoch;
             if (mlist && nmiss < a.miss_cap) mlist[nmiss++] = b;
           }
           stamp[b] = T;
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru_fast(LruArgs ka, LruArgs va
   int32_t* L = a.state + (size_t)u * a.words;
   int32_t* stamp = L + 4;
   int32_t* slot = L + 4 + maxb;  // R == 0
+  int32_t* fresh = L + 4 + 2 * maxb;  // lru_fresh_offset with R == 0
   const int nwork = st.n_work[u];
   const int32_t* work = st.work + (size_t)u * st.wcap;
   __shared__ int ws[32];
@@ -290,6 +294,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru_fast(LruArgs ka, LruArgs va
       if (a.cap > 0) {
         if (miss) {
           slot[b] = count0 + base_m + rank;
+          fresh[b] = st.epoch;
           if (mlist && base_m + rank < a.miss_cap) mlist[base_m + rank] = b;
         }
         stamp[b] = T0 + base_req + roff + nreq - 1;  // stamp of its last request
@@ -400,7 +405,8 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
   for (int kind = 0; kind < 2; ++kind) {
     const int cap = kind ? sc->value_capacity : sc->key_capacity;
     const int R = lru_ring(c->max_blocks, cap);
-    words[kind] = 4 + 2 * c->max_blocks + R;
+    words[kind] = lru_words(c->max_blocks, cap);
+    (void)R;
     la[kind] = LruArgs{*c, *st, kind ? sc->value_lru : sc->key_lru, words[kind], cap, kind, sc->counters,
                        sc->miss_list, sc->miss_n, sc->miss_cap, u0};
     fast = fast && (R == 0);
@@ -420,7 +426,10 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if ((sc->key_slots || sc->value_slots) && sc->miss_list && sc->miss_n) {
+  // Default: pass B reads this step's misses from Tier-2 and fills their slots itself
+  // (the PCIe transfer overlaps pass B); CKV_SEPARATE_PAGEIN=1: gather kernel first.
+  const bool separate = getenv("CKV_SEPARATE_PAGEIN") != nullptr;
+  if (separate && (sc->key_slots || sc->value_slots) && sc->miss_list && sc->miss_n) {
     // page-in on a side stream: forked after the LRU, joined before pass B
     cudaStream_t side = side_stream();
     cudaEvent_t fork, join;
@@ -440,7 +449,7 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
 
 cudaError_t launch_lru_init(int32_t* state, int n_units, int max_blocks, int cap, cudaStream_t s) {
   const int R = lru_ring(max_blocks, cap);
-  const int words = 4 + 2 * max_blocks + R;
+  const int words = lru_words(max_blocks, cap);
   k_lru_init<<<n_units, 256, 0, s>>>(state, words, max_blocks, R);
   return cudaGetLastError();
 }

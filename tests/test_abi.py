@@ -53,8 +53,8 @@ def test_plan_host_only(lib):
     bad = PolicyConfig(exploration_rate=0.0, k_max=600).to_c()
     assert lib.ckv_plan(1, 64, 4, ctypes.byref(bad), ctypes.byref(st)) == 1
     assert lib.ckv_plan(1, 64, 5, ctypes.byref(pol), ctypes.byref(st)) == 1
-    assert lib.ckv_lru_words(8192, 8192) == 4 + 2 * 8192
-    assert lib.ckv_lru_words(8192, 2048) > 4 + 2 * 8192
+    assert lib.ckv_lru_words(8192, 8192) == 4 + 3 * 8192
+    assert lib.ckv_lru_words(8192, 2048) > 4 + 3 * 8192
 
 
 def test_invalid_args_rejected_without_gpu(lib):

@@ -314,11 +314,14 @@ def test_output_soundness_large(ck):
             assert err <= c["e_key_tight"] + c["e_val"] + 1e-5, (u, h, err)
 
 
-def test_host_tier2_matches_device_tier2(ck):
-    """Tier-2 in pinned host RAM (zero-copy reads of promoted originals) gives
-    the same step as Tier-2 in HBM."""
+@pytest.mark.parametrize("env", [{}, {"CKV_SEPARATE_PAGEIN": "1"}], ids=["passb_pagein", "gather_pagein"])
+def test_host_tier2_matches_device_tier2(ck, monkeypatch, env):
+    """Tier-2 in pinned host RAM (misses paged into HBM slots by pass B itself, or
+    by the separate gather kernel) gives the same step as Tier-2 in HBM."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
     cfg = ck.WorkloadConfig(kind="sink", n_tokens=3000, head_dim=128, query_heads=8, kv_heads=2,
-                            steps=2, seed=4)
+                            steps=4, seed=4)
     pol = ck.PolicyConfig(exploration_rate=0.0, v_tol=0.01)
     outs = []
     for where in ("device", "host"):
