@@ -179,10 +179,13 @@ typedef struct {
 
 /* Scratch (LRU page-in) state per unit; capacity in blocks for keys and values.
  * When key_slots / value_slots are given (Tier-2 in pinned host RAM), every
- * miss is copied from Tier-2 into its HBM slot by a gather kernel on a side
- * stream, joined by an event before pass B, which then reads promoted
- * originals from the slots (ScratchCache.request, cache.py:261-286).  Without
- * slots (Tier-2 already in HBM) only the reference accounting runs. */
+ * miss is stamped with st->epoch in the LRU state and copied from Tier-2 into
+ * its HBM slot by pass B as it reads it (or, with CKV_SEPARATE_PAGEIN=1 in the
+ * environment, by a gather kernel on a side stream joined before pass B); pass B
+ * and the dense fallback read resident originals from the slots
+ * (ScratchCache.request, cache.py:261-286).  The caller must change st->epoch
+ * every step.  Without slots (Tier-2 already in HBM) only the reference
+ * accounting runs.  LRU state words per unit: ckv_lru_words(). */
 typedef struct {
   int32_t key_capacity;
   int32_t value_capacity;
