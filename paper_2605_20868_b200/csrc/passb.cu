@@ -53,8 +53,23 @@ __device__ __forceinline__ void vcode_a(uint32_t w, uint32_t& a0, uint32_t& a1, 
 }
 
 // One chunk (IPC consecutive items of unit u's union list, 4 warps interleaved).
+// Page one missed FP16 tile (4 KB) from Tier-2 into its HBM slot, 16 B per lane per
+// group; the caller's lane re-reads exactly the words it wrote.  Out of line: it
+// runs for the few missed items only and keeps pass B's hot loop free of spills.
+__device__ __noinline__ void page_in_tile(const uint16_t* slot, const uint16_t* tier2, int lane) {
+  const uint4* src = reinterpret_cast<const uint4*>(tier2);
+  uint4* dst = reinterpret_cast<uint4*>(const_cast<uint16_t*>(slot));
+  uint4 t[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) t[g] = src[g * 32 + lane];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) dst[g * 32 + lane] = t[g];
+}
+
 // kb = items this warp has pushed through its 2-stage ring so far (stage and
 // mbarrier parity continue across the chunks a persistent CTA processes).
+// SLOTS: the scratch has HBM slots (Tier-2 in host RAM); without them no slot code is compiled in.
+template <bool SLOTS>
 __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, const int u,
                                              const int ck, const int C, int& kb) {
   const ckv_cache& c = a.c;
@@ -97,7 +112,6 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const float p2S = pow2f(Sx);
 
   const size_t ubk = (size_t)u * c.max_blocks;
-  const int maxb = c.max_blocks;
   const int32_t* work = st.work + (size_t)u * st.wcap;
   const float* eta = c.eta + ubk;
   float* lm2 = st.lm2 + ((size_t)u * nh + hq) * c.max_blocks;
@@ -117,8 +131,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const uint8_t* t1base = c.tier1 + ubk * REC;
   // stage = the Tier-1 record (+ the FP16 key tile when some head promotes the block)
   const PageView& pv = a.pv;
-  const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
-  const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
+  const int32_t* kslot = (SLOTS && pv.kslots) ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
+  const int32_t* vslot = (SLOTS && pv.vslots) ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
   // Per-item metadata (work entry, slot, key-scale max, eta, Tier-2 valid,
   // stash epoch) is gathered lane-parallel: lane l holds item j = 32 w + l of
   // the warp's sequence in set w & 1; the set of window w + 2 is refilled at
@@ -143,7 +157,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const int b2 = e2 & 0xffffff;
     int sl = (ok && kslot && (((uint32_t)e2 >> 24) & 0xfu)) ? kslot[b2] : -1;
     // missed into its slot this step: read Tier-2, fill the slot (bit 30 of sl)
-    if (sl >= 0 && kslot[maxb + b2] == st.epoch) sl |= 0x40000000;
+    if (sl >= 0 && kslot[c.max_blocks + b2] == st.epoch) sl |= 0x40000000;
     const float sm = ok ? c.kscale_max[ubk + b2] : 1.f;
     const float et = ok ? eta[b2] : 0.f;
     const int va = ok ? c.tier2_valid[ubk + b2] : 1;
@@ -190,7 +204,6 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   load_words(1);
   int cur = item_at(0);
   int i1 = item_at(1);
-  bool s2g_pending = false;  // lane 0: a slot fill (shared -> global) may be reading a stage
   Meta mc = fetch(0);
   Meta mn = fetch(1);
   if (lane == 0 && cur >= 0) {
@@ -215,8 +228,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     if ((k & 31) == 0 && k >= 32) load_e(((k >> 5) + 1) & 1, k + 32);
     if ((k & 31) == 8 && k >= 32) load_words(((k >> 5) + 1) & 1);
     if (lane == 0 && nxt >= 0) {
-      if (s2g_pending) bulk_wait_read();  // a slot fill may still read the stage
-      s2g_pending = false;
+      if (SLOTS && pv.kslots) bulk_wait_read();  // a slot fill (shared -> global) may still read the stage
       fence_proxy_async();
       issue(mn, stg ^ 1);
     }
@@ -238,10 +250,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const float eta_b = mc.eta;
     mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
     const uint8_t* rec = S.rec[warp][stg];
-    if (fm && mc.sl >= 0 && (mc.sl & 0x40000000) && lane == 0) {  // page-in of a missed key tile
+    if (SLOTS && fm && mc.sl >= 0 && (mc.sl & 0x40000000) && lane == 0) {  // page-in of a missed key tile
       bulk_s2g(const_cast<uint16_t*>(pv.kslots) + ((size_t)u * pv.kcap + (mc.sl & 0x3fffffff)) * B * D,
                S.kt[warp][stg], B * D * 2);
-      s2g_pending = true;
     }
 
     BlockScores r;
@@ -344,17 +355,13 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       split_h2(p4.z, p4.w, h23, l23);
       const uint32_t b0 = lo_lane ? l01 : h01, b1 = lo_lane ? l23 : h23;
       const int vsl = vslot ? vslot[b] : -1;
-      const bool vfill = vsl >= 0 && vslot[maxb + b] == st.epoch;  // missed this step
+      if (vsl >= 0 && vslot[c.max_blocks + b] == st.epoch)  // missed into its slot this step
+        page_in_tile(pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D, c.tier2_v + (ubk + b) * B * D, lane);
       const uint4* vf = reinterpret_cast<const uint4*>(
-          (vsl >= 0 && !vfill) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
+          (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
       uint4 av[NG];
 #pragma unroll
       for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
-      if (vfill) {  // page-in of a missed value tile
-        uint4* dst = reinterpret_cast<uint4*>(const_cast<uint16_t*>(pv.vslots) + ((size_t)u * pv.vcap + vsl) * B * D);
-#pragma unroll
-        for (int g = 0; g < NG; ++g) dst[g * 32 + lane] = av[g];
-      }
 #pragma unroll
       for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, b0, b1);
     }
@@ -365,7 +372,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     mn = fetch(k + 2);
   }
   kb += k;
-  if (lane == 0 && s2g_pending) bulk_wait_all();  // slot fills done before the stages are reused / exit
+  if (SLOTS && lane == 0 && pv.kslots) bulk_wait_all();  // slot fills done before the stages are reused / exit
   if (pv.fused && lane == 0) {
     fold_lru();
     if (lk_h | lk_m | lv_h | lv_m) {
@@ -443,6 +450,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
 
 // Persistent over (unit, chunk) items pulled from a device queue (balanced
 // tail); without st.queue one CTA per (chunk, unit).
+template <bool SLOTS>
 __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
@@ -459,7 +467,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   const int C = st.n_chunks;
   int kb = 0;
   if (!st.queue) {
-    pass_b_chunk(a, S, a.u0 + blockIdx.y, blockIdx.x, C, kb);
+    pass_b_chunk<SLOTS>(a, S, a.u0 + blockIdx.y, blockIdx.x, C, kb);
     return;
   }
   __shared__ int s_item;
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
     const int item = s_item;
     __syncthreads();
     if (item >= total) break;
-    pass_b_chunk(a, S, a.u0 + item / C, item % C, C, kb);
+    pass_b_chunk<SLOTS>(a, S, a.u0 + item / C, item % C, C, kb);
   }
   if (tid == 0) {  // the last CTA out resets the queue for the next launch
     __threadfence();
@@ -664,7 +672,8 @@ extern int g_launches;
 static void passb_attrs() {
   static bool attrs = false;
   if (!attrs) {
-    cudaFuncSetAttribute(k_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
+    cudaFuncSetAttribute(k_pass_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
+    cudaFuncSetAttribute(k_pass_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
     cudaFuncSetAttribute(k_union, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attrs = true;
   }
@@ -684,19 +693,22 @@ cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_st
                          const PageView& pv, int u0, int nu, cudaStream_t s) {
   passb_attrs();
   StepArgs a{*c, *st, *pol, pv, u0, nu};
+  const bool slots_ = pv.kslots || pv.vslots;
   if (st->queue) {
     static int slots = 0;
     if (!slots) {
       int dev = 0, sms = 0, per = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pass_b, PB_WARPS * 32, sizeof(PassBSmem));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pass_b<false>, PB_WARPS * 32, sizeof(PassBSmem));
       slots = max(1, sms * max(1, per));
     }
     const int grid = min(slots, nu * st->n_chunks);
-    k_pass_b<<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+    if (slots_) k_pass_b<true><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+    else k_pass_b<false><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
   } else {
-    k_pass_b<<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+    if (slots_) k_pass_b<true><<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+    else k_pass_b<false><<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
   }
   k_combine<<<dim3(st->n_heads, nu), 128, 0, s>>>(a);
   g_launches += 2;
