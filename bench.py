@@ -84,12 +84,37 @@ def peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML thread
+    polls every ~4 ms between start() and stop() (the timed region is ~20 ms at the
+    default K, too short for nvidia-smi's 200-ms loop); nvidia-smi when NVML is absent."""
 
-    def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index, dev=None):
+        self.index, self.rows, self.proc, self.nv, self.h = index, [], None, None, None
+        try:
+            if os.environ.get("CKV_BENCH_CLOCKS") == "smi":
+                raise ImportError
+            import pynvml
+            pynvml.nvmlInit()
+            try:
+                uuid = str(torch.cuda.get_device_properties(dev).uuid)
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv = pynvml
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.bits = (pynvml.nvmlClocksThrottleReasonHwSlowdown, pynvml.nvmlClocksThrottleReasonHwThermalSlowdown,
+                         pynvml.nvmlClocksThrottleReasonSwThermalSlowdown, pynvml.nvmlClocksThrottleReasonSwPowerCap)
+        except Exception:
+            self.nv = None
 
     def start(self):
+        if self.nv is not None:
+            self.stop_flag = False
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -104,27 +129,41 @@ class ClockSampler:
         self.t = threading.Thread(target=self._read, daemon=True)
         self.t.start()
 
+    def _poll(self):
+        nv = self.nv
+        while not self.stop_flag:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.rows.append([sm, self.smax] + [bool(r & b) for b in self.bits])
+            except Exception:
+                pass
+            time.sleep(0.004)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            if len(parts) == 7 and parts[0].replace(".", "").isdigit():
+                self.rows.append([float(parts[0]), float(parts[1])] + [p == "Active" for p in parts[3:]])
 
     def stop(self):
-        if self.proc is None:
+        if self.nv is not None:
+            self.stop_flag = True
+            self.t.join(timeout=2)
+        elif self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
         rows = list(self.rows)
-        sm = sorted(float(r[0]) for r in rows if r[0].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i] == "Active"})
-        smax = float(rows[0][1]) if rows else None
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax,
-                "reasons": reasons, "samples": len(rows)}
+        sm = sorted(r[0] for r in rows)
+        reasons = sorted({self.NAMES[i] for r in rows for i in range(4) if r[2 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": rows[0][1] if rows else None,
+                "reasons": reasons, "samples": len(rows),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 # -------------------------------------------------------------------------
@@ -350,10 +389,11 @@ def main():
     collect()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(local, dev) if rank == 0 else None
     if sampler:
         sampler.start()
-        time.sleep(0.3)
+        if sampler.nv is None:
+            time.sleep(0.3)  # nvidia-smi start-up
     launches["n"] = 0
     dense_heads["n"] = 0
     stats.update(rung4=0, nv=0.0, pagein=0, steps=0)
