@@ -133,11 +133,19 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   const int nmine = (span > warp) ? (span - warp + PA_WARPS - 1) / PA_WARPS : 0;
   const uint8_t* ubase = c.tier1 + (size_t)u * c.max_blocks * REC;
   const float* smax_u = c.kscale_max + (size_t)u * c.max_blocks;
+#ifdef PA_EVICT_FIRST
+  // the Tier-1 stream is read once: evict it first so what selection and pass B
+  // read next (l'_b, split states, score stash) stays in L2
+  const uint64_t pol_ef = evict_first_policy();
+#define PA_G2S(dst, src, bar) bulk_g2s_hint(dst, src, REC, bar, pol_ef)
+#else
+#define PA_G2S(dst, src, bar) bulk_g2s(dst, src, REC, bar)
+#endif
   if (lane == 0) {
     for (int s = 0; s < PA_STAGES && s < nmine; ++s) {
       int b = b0 + warp + PA_WARPS * s;
       mbar_expect_tx(&S.bar[warp][s], REC);
-      bulk_g2s(S.stage[warp][s], ubase + (size_t)b * REC, REC, &S.bar[warp][s]);
+      PA_G2S(S.stage[warp][s], ubase + (size_t)b * REC, &S.bar[warp][s]);
     }
   }
 
@@ -229,8 +237,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     // proxy fence is needed (write-after-read, no generic writes to order)
     if (lane == 0 && i + PA_STAGES < nmine) {
       mbar_expect_tx(&S.bar[warp][s], REC);
-      bulk_g2s(S.stage[warp][s], ubase + (size_t)(b + PA_WARPS * PA_STAGES) * REC, REC,
-               &S.bar[warp][s]);
+      PA_G2S(S.stage[warp][s], ubase + (size_t)(b + PA_WARPS * PA_STAGES) * REC, &S.bar[warp][s]);
     }
   }
 
