@@ -817,12 +817,45 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
       asm volatile("" ::: "memory");
     }
   }
-  double at = (double)atf, et = (double)etf;
-  tmx = block_max_f(tmx, S.redf);  // largest phase-1 log-mass over the tail
-  at = block_sum_d(at, S.redd);
-  et = block_sum_d(et, S.redd);
-  const int vo = block_excl_scan(nv, S.wsum, &S.misc[7]);
-  const int n_v = S.misc[7];
+  // tail max, the two fp64 sums and the value-list scan in one barrier round; every
+  // thread folds the per-warp partials in warp order (the order block_sum_d uses)
+  double at, et;
+  int vo, n_v;
+  {
+    const float tw = warp_max(tmx);  // largest phase-1 log-mass over the tail
+    const double aw = warp_sum_d((double)atf), ew = warp_sum_d((double)etf);
+    int x = nv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 0) {
+      S.redf[warp] = tw;
+      S.redd[warp] = aw;
+      S.cum[warp] = ew;  // (free after the coverage scan)
+    }
+    if (lane == 31) S.wsum[warp] = x;
+    __syncthreads();
+    float tm = S.redf[0];
+    double ta = 0.0, te = 0.0;
+    int before = 0, tot = 0;
+#pragma unroll 8
+    for (int w = 0; w < NT / 32; ++w) {
+      tm = fmaxf(tm, S.redf[w]);
+      ta += S.redd[w];
+      te += S.cum[w];
+      const int ws = S.wsum[w];
+      before += (w < warp) ? ws : 0;
+      tot += ws;
+    }
+    __syncthreads();
+    tmx = tm;
+    at = ta;
+    et = te;
+    vo = before + x - nv;
+    n_v = tot;
+  }
   {
     int32_t* vlist = st.vlist + hu * c.max_blocks;
     int pv = vo;
