@@ -324,18 +324,15 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
   return r;
 }
 
+// Block reductions: every thread folds the per-warp partials itself, in warp order
+// (so all threads hold the same bits), two barriers per call.
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum_d(v);
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double t = 0.0;
-  if (threadIdx.x == 0) {
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    red[(int)(blockDim.x >> 5)] = t;
-  }
-  __syncthreads();
-  t = red[(int)(blockDim.x >> 5)];
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
   __syncthreads();
   return t;
 }
@@ -345,15 +342,29 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
   v = warp_max(v);
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = red[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, red[w]);
-    red[(int)(blockDim.x >> 5)] = t;
-  }
-  __syncthreads();
-  float t = red[(int)(blockDim.x >> 5)];
+  float t = red[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, red[w]);
   __syncthreads();
   return t;
+}
+
+// two maxima in one barrier round (red: 2 x 32 floats)
+__device__ __forceinline__ float2 block_max_f2(float a, float b, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_max(a);
+  b = warp_max(b);
+  if (lane == 0) {
+    red[warp] = a;
+    red[32 + warp] = b;
+  }
+  __syncthreads();
+  float ta = red[0], tb = red[32];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+    ta = fmaxf(ta, red[w]);
+    tb = fmaxf(tb, red[32 + w]);
+  }
+  __syncthreads();
+  return make_float2(ta, tb);
 }
 
 struct SelSmem {
@@ -461,8 +472,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
       mloc = fmaxf(mloc, sp[0]);
       dloc = fmaxf(dloc, sp[2]);
     }
-    const float M = block_max_f(mloc, S.redf);
-    const float dm = block_max_f(dloc, S.redf);
+    const float2 Mdm = block_max_f2(mloc, dloc, reinterpret_cast<float*>(S.cum));  // S.cum is written below
+    const float M = Mdm.x, dm = Mdm.y;
     for (int s2 = tid; s2 < nsp; s2 += NT) {
       const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
       S.cum[s2] = (sp[0] == ninf()) ? 0.0 : (double)expf(sp[0] - M);
