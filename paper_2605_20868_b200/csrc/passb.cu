@@ -140,11 +140,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   // words), so no load latency sits on the item loop.  Items are fetched from
   // their lane with shuffles two iterations before their copies are issued.
   struct Meta {
-    int e, sl, valid, st;
+    int e, sl, valid, st, vsl;
     float smax, eta;
   };
   const float* stash_u = st.stash ? st.stash + (size_t)u * c.max_blocks * 64 : nullptr;
-  int le[2], lsl[2], lval[2], lsep[2];
+  int le[2], lsl[2], lval[2], lsep[2], lvs[2];
   float lsm[2], let_[2];
   auto load_e = [&](int s, int kbase) {
     const int it = item_at(kbase + lane);
@@ -162,8 +162,14 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const float et = ok ? eta[b2] : 0.f;
     const int va = ok ? c.tier2_valid[ubk + b2] : 1;
     const int se = (ok && stash_u) ? st.stash_epoch[ubk + b2] : 0;
-    if (s) { lsl[1] = sl; lsm[1] = sm; let_[1] = et; lval[1] = va; lsep[1] = se; }
-    else   { lsl[0] = sl; lsm[0] = sm; let_[0] = et; lval[0] = va; lsep[0] = se; }
+    // value slot (bit 30: missed this step), SLOTS instance only
+    int vs = -1;
+    if (SLOTS && vslot && ok && ((uint32_t)e2 >> 28)) {
+      vs = vslot[b2];
+      if (vs >= 0 && vslot[c.max_blocks + b2] == st.epoch) vs |= 0x40000000;
+    }
+    if (s) { lsl[1] = sl; lsm[1] = sm; let_[1] = et; lval[1] = va; lsep[1] = se; lvs[1] = vs; }
+    else   { lsl[0] = sl; lsm[0] = sm; let_[0] = et; lval[0] = va; lsep[0] = se; lvs[0] = vs; }
   };
   auto fetch = [&](int j) -> Meta {  // warp-uniform j
     const int s = (j >> 5) & 1, src = j & 31;
@@ -173,6 +179,7 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     m.smax = __shfl_sync(0xffffffffu, s ? lsm[1] : lsm[0], src);
     m.eta = __shfl_sync(0xffffffffu, s ? let_[1] : let_[0], src);
     m.valid = __shfl_sync(0xffffffffu, s ? lval[1] : lval[0], src);
+    m.vsl = SLOTS ? __shfl_sync(0xffffffffu, s ? lvs[1] : lvs[0], src) : -1;
     const int se = __shfl_sync(0xffffffffu, s ? lsep[1] : lsep[0], src);
     // usable when this step's pass A stashed every head the item is promoted for
     const uint32_t need = (((uint32_t)m.e >> 24) | ((uint32_t)m.e >> 28)) & 0xfu;
@@ -191,6 +198,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
       bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
     }
+    // a value tile missed this step is read from host Tier-2 in the item's value
+    // branch: start pulling it into L2 now
+    if (SLOTS && m.vsl >= 0 && (m.vsl & 0x40000000)) prefetch_l2(c.tier2_v + (ubk + b2) * B * D, B * D * 2);
     if (keys) {
       const uint16_t* src = (m.sl >= 0 && !(m.sl & 0x40000000))
                                 ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
@@ -354,9 +364,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       split_h2(p4.x, p4.y, h01, l01);
       split_h2(p4.z, p4.w, h23, l23);
       const uint32_t b0 = lo_lane ? l01 : h01, b1 = lo_lane ? l23 : h23;
-      const int vsl = vslot ? vslot[b] : -1;
-      if (vsl >= 0 && vslot[c.max_blocks + b] == st.epoch)  // missed into its slot this step
+      int vsl = SLOTS ? mc.vsl : -1;
+      if (vsl >= 0 && (vsl & 0x40000000)) {  // missed into its slot this step
+        vsl &= 0x3fffffff;
         page_in_tile(pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D, c.tier2_v + (ubk + b) * B * D, lane);
+      }
       const uint4* vf = reinterpret_cast<const uint4*>(
           (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
       uint4 av[NG];
