@@ -74,12 +74,19 @@ typedef struct {
   uint16_t* tier2_k;       /* fp16 [n_units][max_blocks*16][128]; device or mapped pinned host */
   uint16_t* tier2_v;
   uint8_t* tier2_valid;    /* [n_units][max_blocks] 1 = originals present */
-  int32_t* status;         /* [8] sticky device error words (see CKV_ST_*) */
+  int32_t* status;         /* [8] device error words (see CKV_ST_*) */
 } ckv_cache;
 
+/* status words.  NONFINITE counts the appends rejected for a non-finite entry
+ * since the last reset (a host compares it with the count it has reported, so
+ * every rejection is reported once, also through deferred checks); CAPACITY is
+ * sticky; TIER2 is per decode step (cleared when the step begins, set by any
+ * kernel of the step that needed a lost Tier-2 block); APPEND_BAD is the
+ * verdict of the append in flight (cleared when it begins). */
 #define CKV_ST_NONFINITE 0
 #define CKV_ST_CAPACITY 1
 #define CKV_ST_TIER2 2
+#define CKV_ST_APPEND_BAD 3
 
 typedef struct {
   double tau_cov;

@@ -20,7 +20,7 @@ SPLIT_FLOATS = 136
 HEAD_FLOATS = 288
 CHUNK_FLOATS = 136
 
-ST_NONFINITE, ST_CAPACITY, ST_TIER2 = 0, 1, 2
+ST_NONFINITE, ST_CAPACITY, ST_TIER2, ST_APPEND_BAD = 0, 1, 2, 3
 
 F_RUNG1, F_RUNG2, F_RANKING, F_BOUNDARY = 1, 2, 4, 8
 F_CANARY, F_CLAMPED, F_NUMERIC, F_ACTIVE = 16, 32, 64, 128

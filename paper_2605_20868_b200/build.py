@@ -1,15 +1,21 @@
-"""In-tree build of libcertkv_b200.so for sm_100a (nvcc, no JIT cache)."""
+"""In-tree build of libcertkv_b200.so for sm_100a (nvcc, no JIT cache).
+
+Every ``csrc/*.cu`` is compiled to an object in parallel (the kernels of one
+file never call device code of another), then the objects are linked into the
+shared library next to this file."""
 
 import glob
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libcertkv_b200.so")
-NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+OBJ = os.path.join(HERE, "build")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
 
 
 def sources():
@@ -21,7 +27,7 @@ def needs_build():
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + \
-        [os.path.join(ROOT, "include", "certkv_b200.h")]
+        [os.path.join(ROOT, "include", "certkv_b200.h"), os.path.abspath(__file__)]
     return any(os.path.getmtime(p) > t for p in deps)
 
 
@@ -36,11 +42,24 @@ def build(force=False, verbose=False):
             return LIB
         nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
         extra = os.environ.get("CKV_NVCC_EXTRA", "").split()  # experiments only (e.g. -DPA_MINB=4)
-        tmp = f"{LIB}.{os.getpid()}.tmp"
-        cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
+        os.makedirs(OBJ, exist_ok=True)
+        tag = os.getpid()
+
+        def compile_one(src):
+            obj = os.path.join(OBJ, os.path.basename(src)[:-3] + f".{tag}.o")
+            cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-c", src,
+                   "-o", obj]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.run(cmd, check=True)
+            return obj
+
+        with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+            objs = list(ex.map(compile_one, sources()))
+        tmp = f"{LIB}.{tag}.tmp"
+        subprocess.run([nvcc, *ARCH, "-shared", *objs, "-o", tmp], check=True)
+        for o in objs:
+            os.remove(o)
         os.replace(tmp, LIB)
     return LIB
 

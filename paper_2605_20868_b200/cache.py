@@ -12,7 +12,8 @@ HBM layout per unit (see include/certkv_b200.h):
 """
 
 import ctypes
-from dataclasses import dataclass
+import weakref
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -104,6 +105,8 @@ class DeviceKVCache:
             tier2_k=_ptr(self.tier2_k), tier2_v=_ptr(self.tier2_v),
             tier2_valid=_ptr(self.tier2_valid), status=_ptr(self.status))
         self._tokens = 0  # host mirror: every unit receives the same appends
+        self._nonfinite_reported = 0  # rejected appends already raised (status word 0)
+        self._scratches = weakref.WeakSet()  # ScratchCaches bound to this cache
 
     # -- shape ------------------------------------------------------------
     @property
@@ -166,8 +169,7 @@ class DeviceKVCache:
         _lib.check(code, "ckv_append")
         if validate and not defer:
             st = self.status.cpu()
-            if st[_lib.ST_NONFINITE]:
-                self.status[_lib.ST_NONFINITE] = 0
+            if self.take_rejections(st):
                 raise ValueError("non-finite key/value entry")
             if st[_lib.ST_CAPACITY]:
                 raise ValueError("cache capacity exceeded")
@@ -185,10 +187,25 @@ class DeviceKVCache:
         _lib.check(code, "ckv_f64_to_f16")
         return y
 
+    def take_rejections(self, status):
+        """True if ``status`` (a host copy of the status words) shows appends
+        rejected for a non-finite entry that were not reported yet; marks them
+        reported, so every rejection raises exactly once."""
+        n = int(status[_lib.ST_NONFINITE])
+        if n > self._nonfinite_reported:
+            self._nonfinite_reported = n
+            return True
+        return False
+
     def reset(self):
+        """Empty every unit.  LRU scratches bound to this cache are re-initialised
+        (nothing stays resident), so a refilled cache never hits stale slots."""
         _lib.check(self.lib.ckv_reset(ctypes.byref(self.c), _stream(self.device)), "ckv_reset")
         self.tier2_valid.zero_()
         self._tokens = 0
+        self._nonfinite_reported = 0
+        for sc in list(self._scratches):
+            sc._init_device(self)
 
     # -- reads / parity views ------------------------------------------------
     def read_tier1(self, unit, b0=0, nb=None):
@@ -256,9 +273,29 @@ class DeviceKVCache:
                 "cannot serve a fallback or promotion")
 
 
+@dataclass
+class PageInReport:
+    """Accounting outcome of one promotion request (cache.py:230-240).  The
+    device keeps the payloads in HBM, so ``payloads`` stays empty."""
+    hits: int = 0
+    misses: int = 0
+    bytes: int = 0
+    payloads: dict = field(default_factory=dict, repr=False)
+
+    def to_dict(self):
+        return {"hits": self.hits, "misses": self.misses, "bytes": self.bytes}
+
+
 class ScratchCache:
     """LRU accounting + capacity for promoted originals of every unit, on device
-    (cache.py:243-291 semantics; ckv_scratch in the C ABI)."""
+    (cache.py:243-291 semantics; ckv_scratch in the C ABI).
+
+    Bound to a DeviceKVCache (``CertifiedDecoder(..., scratch=)``) it holds the
+    key LRU (``capacity``) and the value LRU (``value_capacity``) of every unit.
+    Used the reference way -- one ScratchCache per payload kind passed to
+    ``run_decode_step(key_scratch=, value_scratch=)`` -- it is the accounting
+    view of that kind: ``hits`` / ``misses`` / ``bytes_paged_in`` / ``hit_rate``
+    count the requests made through it."""
 
     def __init__(self, capacity, value_capacity=None):
         if capacity < 0 or (value_capacity is not None and value_capacity < 0):
@@ -266,11 +303,17 @@ class ScratchCache:
         self.capacity = int(capacity)
         self.value_capacity = int(capacity if value_capacity is None else value_capacity)
         self._bound = None
+        self._acc = [0, 0, 0]  # hits, misses, bytes as a single-kind view (unbound)
+
+    def _account(self, hits, misses, nbytes):
+        self._acc[0] += int(hits)
+        self._acc[1] += int(misses)
+        self._acc[2] += int(nbytes)
 
     def bind(self, cache, n_heads=4, kcap=258):
         """Allocate the device LRU state (and, with Tier-2 in host RAM, the HBM
         slot pool + miss lists of the side-stream page-in) for ``cache``."""
-        if self._bound is cache:
+        if self._bound is not None and self._bound() is cache:
             return
         lib = cache.lib
         U, NB = cache.n_units, cache.max_blocks
@@ -297,12 +340,19 @@ class ScratchCache:
                                  counters=_ptr(self.counters), key_slots=_ptr(self.key_slots),
                                  value_slots=_ptr(self.value_slots), miss_list=_ptr(self.miss_list),
                                  miss_n=_ptr(self.miss_n), miss_cap=miss_cap)
-        _lib.check(lib.ckv_scratch_init(U, NB, ctypes.byref(self.c), _stream(dev)),
-                   "ckv_scratch_init")
-        self._bound = cache
+        self._init_device(cache)
+        self._bound = weakref.ref(cache)
+        cache._scratches.add(self)
+
+    def _init_device(self, cache):
+        """Empty LRU (nothing resident) and zero counters."""
+        _lib.check(cache.lib.ckv_scratch_init(cache.n_units, cache.max_blocks, ctypes.byref(self.c),
+                                              _stream(cache.device)), "ckv_scratch_init")
 
     def totals(self):
         """(key hits, key misses, key bytes, value hits, value misses, value bytes)."""
+        if self._bound is None:
+            return [*self._acc, 0, 0, 0]
         return self.counters.sum(0).cpu().tolist()
 
     @property
@@ -333,12 +383,16 @@ class TieredCache:
     Storage is FP16 (binary16 ingest, cache.py:82-84).
     """
 
-    def __init__(self, block_size, head_dim, group_size=16, ingest_binary16=True,
+    def __init__(self, block_size, head_dim, group_size=16, ingest_binary16=False,
                  max_tokens=65536, device="cuda", tier2="device"):
         if head_dim % group_size != 0:
             raise ValueError(f"group size {group_size} does not divide head dim {head_dim}")
         if (block_size, head_dim, group_size) != (B, D, G):
             raise ValueError("the device path supports block_size=16, head_dim=128, group_size=16")
+        if not ingest_binary16:
+            # the reference default keeps float32 originals (cache.py:52, 82-84); the
+            # device keeps FP16 Tier-2 only, so refuse rather than round silently
+            raise ValueError("the device path stores FP16 originals: pass ingest_binary16=True")
         self.block_size, self.head_dim, self.group_size = B, D, G
         self.ingest_binary16 = True
         self.dev = DeviceKVCache(1, max_tokens, device=device, tier2=tier2)

@@ -1,9 +1,61 @@
 // extern "C" entry points of libcertkv_b200.so (declared in include/certkv_b200.h).
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
 #include "common.cuh"
 
 namespace ckv {
-extern int g_launches;
+const Knobs& knobs() {
+  static const Knobs k = [] {
+    Knobs r;
+    r.separate_lru = getenv("CKV_SEPARATE_LRU") != nullptr;
+    r.separate_pagein = getenv("CKV_SEPARATE_PAGEIN") != nullptr;
+    const char* ch = getenv("CKV_CHUNKS");
+    r.chunks = ch ? atoi(ch) : 1;
+    return r;
+  }();
+  return k;
+}
+
+static std::mutex g_dev_mu;
+static DevState g_dev[64];
+
+DevState& dev_state() {
+  int d = 0;
+  cudaGetDevice(&d);
+  DevState& ds = g_dev[d & 63];
+  if (!ds.sms) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    if (!ds.sms) {
+      int lo = 0, hi = 0, sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&ds.tail, cudaStreamNonBlocking, hi);
+      cudaStreamCreateWithFlags(&ds.side, cudaStreamNonBlocking);
+      ds.sms = sms > 0 ? sms : 148;
+    }
+  }
+  return ds;
+}
+
+cudaError_t set_max_dyn_smem_fn(const void* fn, int bytes) {
+  DevState& ds = dev_state();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  for (int i = 0; i < ds.n_attr; ++i)
+    if (ds.attr_fn[i] == fn) {
+      if (ds.attr_bytes[i] >= bytes) return cudaSuccess;
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) ds.attr_bytes[i] = bytes;
+      return e;
+    }
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && ds.n_attr < 32) {
+    ds.attr_fn[ds.n_attr] = fn;
+    ds.attr_bytes[ds.n_attr] = bytes;
+    ++ds.n_attr;
+  }
+  return e;
+}
 cudaError_t launch_append(const ckv_cache*, const uint16_t*, const uint16_t*, int32_t, cudaStream_t);
 cudaError_t launch_read_tier1(const ckv_cache*, int, int, int, int8_t*, float*, float*, uint8_t*,
                               uint16_t*, uint16_t*, cudaStream_t);
@@ -121,6 +173,9 @@ ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step*
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   if (scratch && (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters))
     return CKV_EINVAL;
+  // Tier-2 loss is reported per step
+  cudaError_t e = cudaMemsetAsync(c->status + CKV_ST_TIER2, 0, sizeof(int32_t), S(stream));
+  if (e != cudaSuccess) return st_of(e);
   return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, S(stream)));
 }
 

@@ -81,6 +81,37 @@ __host__ __device__ inline int v2_offset(int t, int c) {
   return g * 256 + lane * 8 + reg * 2 + (t & 1);
 }
 
+// ---- host-side runtime state (capi.cu) ----------------------------------------
+// Function attributes, occupancy-derived grid sizes and auxiliary streams are
+// per device (one process may drive several GPUs); the A/B environment knobs are
+// read once per process.
+struct Knobs {
+  bool separate_lru;     // CKV_SEPARATE_LRU: k_lru_fast instead of the LRU fused into pass B
+  bool separate_pagein;  // CKV_SEPARATE_PAGEIN: gather kernel on a side stream before pass B
+  int chunks;            // CKV_CHUNKS: unit-chunked overlap of the tail with pass A
+};
+const Knobs& knobs();
+struct DevState {
+  int sms = 0;
+  int dense_slots = 0;
+  int passb_slots = 0;
+  cudaStream_t tail = nullptr;  // high priority
+  cudaStream_t side = nullptr;  // page-in
+  int n_attr = 0;
+  const void* attr_fn[32] = {};
+  int attr_bytes[32] = {};
+};
+DevState& dev_state();  // of the current device
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `fn` on the current device
+// (set once per device and size)
+cudaError_t set_max_dyn_smem_fn(const void* fn, int bytes);
+template <class F>
+inline cudaError_t set_max_dyn_smem(F* fn, int bytes) {
+  return set_max_dyn_smem_fn(reinterpret_cast<const void*>(fn), bytes);
+}
+constexpr size_t kLruSmemMax = 227 * 1024;
+extern thread_local int g_launches;  // kernels launched by the last C-ABI call of this thread
+
 // LRU ring size for a scratch of `cap` blocks (0 = no eviction possible); see scratch.cu
 __host__ __device__ inline int lru_ring(int max_blocks, int cap) {
   if (cap >= max_blocks) return 0;
@@ -89,8 +120,14 @@ __host__ __device__ inline int lru_ring(int max_blocks, int cap) {
   while (R < need) R <<= 1;
   return R;
 }
+// words of an evicting k_lru's work arrays (request list, compaction buffer,
+// bitmap) kept behind the state for units too large for shared memory
+__host__ __device__ inline int lru_work_words(int max_blocks) {
+  return 2 * max_blocks + 1024 + (max_blocks + 31) / 32 + 4;
+}
 __host__ __device__ inline int lru_words(int max_blocks, int cap) {
-  return 4 + 3 * max_blocks + lru_ring(max_blocks, cap);
+  const int R = lru_ring(max_blocks, cap);
+  return 4 + 3 * max_blocks + R + (R ? lru_work_words(max_blocks) : 0);
 }
 // per-block epoch of the step that missed it into its slot (the slot is filled by
 // that step's pass B, or by k_pagein); = slot table + max_blocks

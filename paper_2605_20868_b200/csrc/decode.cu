@@ -961,7 +961,6 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // =============================================================================
 // launchers
 // =============================================================================
-extern int g_launches;
 cudaError_t launch_union(const ckv_cache*, const ckv_policy*, const ckv_step*, int, int, cudaStream_t);
 cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&, int, int,
                          cudaStream_t);
@@ -1004,7 +1003,7 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
     const bool fuse = lru_ring(c->max_blocks, sc->key_capacity) == 0 &&
                       lru_ring(c->max_blocks, sc->value_capacity) == 0 && sc->key_capacity > 0 &&
                       sc->value_capacity > 0 && !sc->key_slots && !sc->value_slots &&
-                      !getenv("CKV_SEPARATE_LRU");
+                      !knobs().separate_lru;
     if (fuse) {
       cudaMemsetAsync(st->page_stats + (size_t)u0 * 4, 0, sizeof(int32_t) * 4 * nu, s);
       pv.fused = 1;
@@ -1028,16 +1027,6 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   return launch_passb(c, pol, st, pv, u0, nu, s);
 }
 
-static cudaStream_t tail_stream() {  // high priority: tail kernels jump ahead of pass-A CTAs
-  static cudaStream_t s = nullptr;
-  if (!s) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi);
-  }
-  return s;
-}
-
 // Optional unit chunks (CKV_CHUNKS=n): pass A of chunk k+1 runs while the
 // tail of chunk k runs on a second, high-priority stream.  Units are
 // independent, so the result is identical to one launch over all units.  Off
@@ -1045,8 +1034,7 @@ static cudaStream_t tail_stream() {  // high priority: tail kernels jump ahead o
 // registers), so tail CTAs displace pass-A CTAs instead of filling gaps
 // (measured at C3: 1 chunk 2.47 ms, 2 chunks 2.53, 4 chunks 2.69).
 static int decode_chunks(int n_units) {
-  const char* env = getenv("CKV_CHUNKS");
-  int n = env ? atoi(env) : 1;
+  int n = knobs().chunks;
   if (n_units < 16) n = 1;
   return max(1, min(n, n_units));
 }
@@ -1055,22 +1043,21 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
                           const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
   g_launches = 0;
   const size_t smA = sizeof(PassASmem);
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(k_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
-    cudaFuncSetAttribute(k_select<8, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<8, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<16, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<32, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<64, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_select<128, SEL_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attrs = true;
+  set_max_dyn_smem(k_pass_a, (int)smA);
+  {
+    const int smS = (int)(sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4);
+    set_max_dyn_smem(k_select<8, 1024>, smS);
+    set_max_dyn_smem(k_select<8, SEL_THREADS>, smS);
+    set_max_dyn_smem(k_select<16, SEL_THREADS>, smS);
+    set_max_dyn_smem(k_select<32, SEL_THREADS>, smS);
+    set_max_dyn_smem(k_select<64, SEL_THREADS>, smS);
+    set_max_dyn_smem(k_select<128, SEL_THREADS>, smS);
   }
   const int U = c->n_units;
   const int nch = decode_chunks(U);
   const int per = (U + nch - 1) / nch;
   const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
-  cudaStream_t s2 = (nch > 1) ? tail_stream() : s;
+  cudaStream_t s2 = (nch > 1) ? dev_state().tail : s;
   cudaError_t e = cudaSuccess;
   if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
   cudaEvent_t evs[64];

@@ -279,7 +279,6 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   }  // task loop
 }
 
-extern int g_launches;
 
 cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStream_t s) {
   DenseArgs a{*c, *st, 0, 0, 0, PageView{}};
@@ -304,14 +303,13 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scrat
     a.pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
     a.pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
   }
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  DevState& ds = dev_state();
+  if (!ds.dense_slots) {
+    int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dense, DN_WARPS * 32, 0);
-    slots = max(1, sms * max(1, per));
+    ds.dense_slots = max(1, ds.sms * max(1, per));
   }
+  const int slots = ds.dense_slots;
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t) * (1 + c->n_units), s);  // count + done counters
   k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
   k_dense<<<slots, DN_WARPS * 32, 0, s>>>(a);

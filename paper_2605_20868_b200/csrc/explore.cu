@@ -85,7 +85,6 @@ __global__ void __launch_bounds__(128) k_explore(StepArgs a) {
   }
 }
 
-extern int g_launches;
 
 cudaError_t launch_explore(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                            int host_max_blocks, cudaStream_t s) {

@@ -51,7 +51,7 @@ __global__ void k_check_finite(const uint4* k, const uint4* v, size_t n16, int32
       bad |= ((w[j] & 0x7c00u) == 0x7c00u) | ((w[j] & 0x7c000000u) == 0x7c000000u);
     }
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status[CKV_ST_NONFINITE], 1);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&status[CKV_ST_APPEND_BAD], 1);
 }
 
 struct FillArgs {
@@ -64,7 +64,7 @@ struct FillArgs {
 __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
   const ckv_cache& c = a.c;
   const int u = blockIdx.y, j = blockIdx.x, tid = threadIdx.x;
-  if (c.status[CKV_ST_NONFINITE]) return;
+  if (c.status[CKV_ST_APPEND_BAD]) return;  // the whole append is rejected
   const int p = c.partial_len[u];
   const int nf = (p + a.n_tok) / B;
   if (j >= nf) return;
@@ -205,7 +205,10 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
 __global__ void k_tail(FillArgs a) {
   const ckv_cache& c = a.c;
   const int u = blockIdx.x, tid = threadIdx.x;
-  if (c.status[CKV_ST_NONFINITE]) return;
+  if (c.status[CKV_ST_APPEND_BAD]) {  // rejected: count it once, mutate nothing
+    if (u == 0 && tid == 0) atomicAdd(&c.status[CKV_ST_NONFINITE], 1);
+    return;
+  }
   const int p = c.partial_len[u];
   const int total = p + a.n_tok;
   const int nf = total / B;
@@ -276,7 +279,7 @@ __global__ void k_reset(ckv_cache c) {
 // ---------------------------------------------------------------------------
 // launch wrappers used by capi.cu
 namespace ckv {
-int g_launches = 0;
+thread_local int g_launches = 0;
 
 cudaError_t launch_append(const ckv_cache* c, const uint16_t* k_new, const uint16_t* v_new,
                           int32_t n_tok, cudaStream_t s) {
@@ -285,6 +288,7 @@ cudaError_t launch_append(const ckv_cache* c, const uint16_t* k_new, const uint1
   int grid = (int)((n16 + 255) / 256);
   if (grid > 4 * 148 * 8) grid = 4 * 148 * 8;
   if (grid < 1) grid = 1;
+  cudaMemsetAsync(c->status + CKV_ST_APPEND_BAD, 0, sizeof(int32_t), s);
   k_check_finite<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(k_new),
                                       reinterpret_cast<const uint4*>(v_new), n16, c->status);
   ++g_launches;

@@ -679,21 +679,16 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   }
 }
 
-extern int g_launches;
 
-static void passb_attrs() {
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(k_pass_b<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
-    cudaFuncSetAttribute(k_pass_b<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PassBSmem));
-    cudaFuncSetAttribute(k_union, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attrs = true;
-  }
+static void passb_attrs(const ckv_cache* c) {
+  set_max_dyn_smem(k_pass_b<false>, (int)sizeof(PassBSmem));
+  set_max_dyn_smem(k_pass_b<true>, (int)sizeof(PassBSmem));
+  set_max_dyn_smem(k_union, 2 * H * ((c->max_blocks + 31) / 32) * 4);
 }
 
 cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st, int u0, int nu,
                          cudaStream_t s) {
-  passb_attrs();
+  passb_attrs(c);
   StepArgs a{*c, *st, *pol, PageView{}, u0};
   const int W = (c->max_blocks + 31) / 32;
   k_union<<<nu, UN_THREADS, 2 * H * W * 4, s>>>(a);
@@ -703,18 +698,17 @@ cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_st
 
 cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                          const PageView& pv, int u0, int nu, cudaStream_t s) {
-  passb_attrs();
+  passb_attrs(c);
   StepArgs a{*c, *st, *pol, pv, u0, nu};
   const bool slots_ = pv.kslots || pv.vslots;
   if (st->queue) {
-    static int slots = 0;
-    if (!slots) {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    DevState& ds = dev_state();
+    if (!ds.passb_slots) {
+      int per = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pass_b<false>, PB_WARPS * 32, sizeof(PassBSmem));
-      slots = max(1, sms * max(1, per));
+      ds.passb_slots = max(1, ds.sms * max(1, per));
     }
+    const int slots = ds.passb_slots;
     const int grid = min(slots, nu * st->n_chunks);
     if (slots_) k_pass_b<true><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
     else k_pass_b<false><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);

@@ -63,6 +63,7 @@ struct LruArgs {
   int32_t* miss_n;     // [U][2]
   int32_t miss_cap;
   int32_t u0;
+  int32_t gmem;  // 1: state too large for shared memory, work on it in global memory
 };
 
 __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
@@ -82,18 +83,31 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   __syncthreads();
   const int R = hdr[3];
   const int M = R - 1;
-  int32_t* stamp = sm;               // [maxb]
-  int32_t* ring = sm + maxb;         // [R]
-  int32_t* slot = ring + R;          // [maxb]
-  int32_t* req = slot + maxb;        // [maxb + 1024] request list
-  int32_t* tmp = req + maxb + 1024;  // [maxb] compaction buffer
-  uint32_t* bits = reinterpret_cast<uint32_t*>(tmp + maxb);  // [maxb/32]
-  const int32_t* Lslot = L + 4 + maxb + R;
-  for (int i = tid; i < maxb; i += LRU_THREADS) {
-    stamp[i] = (i < nb) ? L[4 + i] : 0;
-    slot[i] = (i < nb) ? Lslot[i] : -1;
+  // the state (stamp, ring, slot) and the work arrays live in shared memory when
+  // they fit (a.gmem == 0); otherwise the kernel works on the global state in
+  // place, with the work arrays behind it (lru_work_words)
+  int32_t *stamp, *ring, *slot, *req, *tmp;
+  if (!a.gmem) {
+    stamp = sm;               // [maxb]
+    ring = sm + maxb;         // [R]
+    slot = ring + R;          // [maxb]
+    req = slot + maxb;        // [maxb + 1024] request list
+  } else {
+    stamp = L + 4;
+    ring = L + 4 + maxb;
+    slot = ring + R;
+    req = L + lru_fresh_offset(maxb, a.cap) + maxb;
   }
-  for (int i = tid; i < R; i += LRU_THREADS) ring[i] = L[4 + maxb + i];
+  tmp = req + maxb + 1024;  // [maxb] compaction buffer
+  uint32_t* bits = reinterpret_cast<uint32_t*>(tmp + maxb);  // [maxb/32]
+  if (!a.gmem) {
+    const int32_t* Lslot = L + 4 + maxb + R;
+    for (int i = tid; i < maxb; i += LRU_THREADS) {
+      stamp[i] = (i < nb) ? L[4 + i] : 0;
+      slot[i] = (i < nb) ? Lslot[i] : -1;
+    }
+    for (int i = tid; i < R; i += LRU_THREADS) ring[i] = L[4 + maxb + i];
+  }
   __syncthreads();
   int T = hdr[0], P = hdr[1], count = hdr[2];
   const int cap = a.cap;
@@ -233,12 +247,14 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
     __syncthreads();
   }
   // ---- write back ---------------------------------------------------------------
-  int32_t* Ls = L + 4 + maxb + R;
-  for (int i = tid; i < nb; i += LRU_THREADS) {
-    L[4 + i] = stamp[i];
-    Ls[i] = slot[i];
+  if (!a.gmem) {
+    int32_t* Ls = L + 4 + maxb + R;
+    for (int i = tid; i < nb; i += LRU_THREADS) {
+      L[4 + i] = stamp[i];
+      Ls[i] = slot[i];
+    }
+    for (int i = tid; i < R; i += LRU_THREADS) L[4 + maxb + i] = ring[i];
   }
-  for (int i = tid; i < R; i += LRU_THREADS) L[4 + maxb + i] = ring[i];
   if (tid == 0) {
     L[0] = T;
     L[1] = P;
@@ -389,13 +405,6 @@ __global__ void k_lru_init(int32_t* state, int words, int maxb, int R) {
   }
 }
 
-extern int g_launches;
-
-static cudaStream_t side_stream() {
-  static cudaStream_t s = nullptr;
-  if (!s) cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-  return s;
-}
 
 cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc, int u0, int nu,
                            cudaStream_t s) {
@@ -408,7 +417,7 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
     words[kind] = lru_words(c->max_blocks, cap);
     (void)R;
     la[kind] = LruArgs{*c, *st, kind ? sc->value_lru : sc->key_lru, words[kind], cap, kind, sc->counters,
-                       sc->miss_list, sc->miss_n, sc->miss_cap, u0};
+                       sc->miss_list, sc->miss_n, sc->miss_cap, u0, 0};
     fast = fast && (R == 0);
   }
   if (fast) {  // no eviction possible for either kind: one light pass over the union list
@@ -417,9 +426,13 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
   } else {
     for (int kind = 0; kind < 2; ++kind) {
       const int R = lru_ring(c->max_blocks, la[kind].cap);
-      const size_t smem = (size_t)(c->max_blocks + R + c->max_blocks + c->max_blocks + 1024 +
-                                   c->max_blocks + (c->max_blocks + 31) / 32 + 4) * 4;
-      cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      size_t smem = (size_t)(c->max_blocks + R + c->max_blocks + lru_work_words(c->max_blocks)) * 4;
+      if (smem > kLruSmemMax) {
+        la[kind].gmem = 1;
+        smem = 0;
+      } else {
+        set_max_dyn_smem(k_lru, (int)smem);
+      }
       k_lru<<<nu, LRU_THREADS, smem, s>>>(la[kind]);
       ++g_launches;
     }
@@ -428,10 +441,10 @@ cudaError_t launch_scratch(const ckv_cache* c, const ckv_step* st, const ckv_scr
   if (e != cudaSuccess) return e;
   // Default: pass B reads this step's misses from Tier-2 and fills their slots itself
   // (the PCIe transfer overlaps pass B); CKV_SEPARATE_PAGEIN=1: gather kernel first.
-  const bool separate = getenv("CKV_SEPARATE_PAGEIN") != nullptr;
+  const bool separate = knobs().separate_pagein;
   if (separate && (sc->key_slots || sc->value_slots) && sc->miss_list && sc->miss_n) {
     // page-in on a side stream: forked after the LRU, joined before pass B
-    cudaStream_t side = side_stream();
+    cudaStream_t side = dev_state().side;
     cudaEvent_t fork, join;
     cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&join, cudaEventDisableTiming);

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .cache import DeviceKVCache, ScratchCache, TieredCache, _ptr, _stream
+from .cache import DeviceKVCache, PageInReport, ScratchCache, TieredCache, _ptr, _stream
 from .errors import EmptyCacheError, Tier2UnavailableError
 from .policy import (KINDS, RETURNED_DENSE_ALL_HEADS, RETURNED_QUANTIZED, Certificate,
                      PolicyConfig, RungFlags, events_from_flags)
@@ -60,16 +60,26 @@ class PendingStep:
 
     def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens):
         self._args = (cert_h, stat_h, ps_h, n_tokens)
-        self._dec, self._ev, self._res = dec, event, None
+        self._dec, self._ev, self._res, self._exc = dec, event, None, None
 
     def done(self):
         return self._ev.query()
 
+    def _decode(self):
+        """Decode the pinned copies once; an error (Tier-2 loss, a rejected
+        deferred append) is kept and raised by ``result()`` of this step."""
+        if self._res is None and self._exc is None:
+            self._ev.synchronize()
+            try:
+                self._res = self._dec._output(*self._args)
+            except (ValueError, Tier2UnavailableError) as e:
+                self._exc = e
+
     def result(self):
         """Wait for this step's certificates (not for later steps) and decode them."""
-        if self._res is None:
-            self._ev.synchronize()
-            self._res = self._dec._output(*self._args)
+        self._decode()
+        if self._exc is not None:
+            raise self._exc
         return self._res
 
 
@@ -228,7 +238,7 @@ class CertifiedDecoder:
             self._ring_pending = [None, None]
         prev = self._ring_pending[k]
         if prev is not None:
-            prev.result()  # decode the step that last used this buffer before reusing it
+            prev._decode()  # decode the step that last used this buffer before reusing it
         cert_h, stat_h, ps_h, ev = self._ring[k]
         cert_h.copy_(self.cert_buf, non_blocking=True)
         stat_h.copy_(self.cache.status, non_blocking=True)
@@ -248,12 +258,10 @@ class CertifiedDecoder:
         return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens)
 
     def _output(self, cert_h, stat_h, ps_h, n_tokens):
-        if stat_h[_lib.ST_NONFINITE]:  # a deferred append check (DeviceKVCache.append)
-            self.cache.status[_lib.ST_NONFINITE] = 0
+        if self.cache.take_rejections(stat_h):  # a deferred append check (DeviceKVCache.append)
             self.cache.resync()
             raise ValueError("non-finite key/value entry (append rejected on the device)")
-        if stat_h[_lib.ST_TIER2]:
-            self.cache.status[_lib.ST_TIER2] = 0
+        if stat_h[_lib.ST_TIER2]:  # per-step word: this step needed a lost block
             raise Tier2UnavailableError("full-precision originals of a promoted block are unavailable")
         cert = cert_h.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh).copy()
         kinds = cert["returned_kind"].copy()
@@ -356,31 +364,38 @@ def run_decode_step(query, cache, policy, key_scratch=None, value_scratch=None, 
         raise ValueError(f"query has length {q.shape[0]}, expected {cache.head_dim}")
     scratch = None
     if key_scratch is not None or value_scratch is not None:
+        # one device LRU state per (key scratch, value scratch) pair, held by the
+        # cache (with the pair, so the ids stay unique while it lives); the
+        # caller's objects receive the per-kind accounting of every request
         kc = key_scratch.capacity if key_scratch is not None else 1 << 30
         vc = value_scratch.capacity if value_scratch is not None else 1 << 30
-        key = ("scr", id(key_scratch), id(value_scratch))
-        scratch = cache.__dict__.setdefault(key, ScratchCache(kc, vc))
+        reg = cache.__dict__.setdefault("_scratch_pairs", {})
+        key = (id(key_scratch), id(value_scratch))
+        if key not in reg:
+            reg[key] = (key_scratch, value_scratch, ScratchCache(kc, vc))
+        scratch = reg[key][2]
     dkey = ("dec", policy, id(scratch))
     dec = cache.__dict__.get(dkey)
     if dec is None:
         dec = CertifiedDecoder(cache.dev, policy, n_heads=1, scratch=scratch)
         cache.__dict__[dkey] = dec
-    before = scratch.counters.sum(0).cpu().tolist() if scratch is not None else None
     res = dec.step(torch.from_numpy(q).reshape(1, 1, D).to(cache.dev.device), rng=rng)
     row = res.cert[0, 0]
     kind = int(res.kinds[0, 0])
     cert = certificate_from_row(row, head, step, kind)
     reports = {}
     if scratch is not None:
-        after = scratch.counters.sum(0).cpu().tolist()
-        d = [a - b for a, b in zip(after, before)]
+        ps = res.page_stats[0]  # this step's (key hits, key misses, value hits, value misses)
+        nbytes = B * D * 2
         if key_scratch is not None:
-            reports["keys"] = {"hits": d[0], "misses": d[1], "bytes": d[2]}
+            reports["keys"] = PageInReport(int(ps[0]), int(ps[1]), int(ps[1]) * nbytes)
+            key_scratch._account(ps[0], ps[1], int(ps[1]) * nbytes)
         if value_scratch is not None:
-            reports["values"] = {"hits": d[3], "misses": d[4], "bytes": d[5]}
+            reports["values"] = PageInReport(int(ps[2]), int(ps[3]), int(ps[3]) * nbytes)
+            value_scratch._account(ps[2], ps[3], int(ps[3]) * nbytes)
     if res.explore_counts is not None:
         n = int(res.explore_counts[0, 0])
-        reports["exploration"] = {"hits": 0, "misses": n, "bytes": n * B * D * 2}
+        reports["exploration"] = PageInReport(0, n, n * B * D * 2)
     prom = res.promoted(0, 0)
     vprom = frozenset(int(b) for b in res.value_promotions(0, 0))
     decision = SelectionView(frozenset(int(b) for b in prom), int(row["k_star"]),

@@ -24,16 +24,23 @@ WORKLOAD_KINDS = ("gaussian", "sink", "needle", "near_tie")
 
 @dataclass(frozen=True)
 class WorkloadConfig:
+    """Fields and defaults of the reference WorkloadConfig (harness.py:41-81).
+
+    The device path runs head_dim 128, block 16, group 16 with FP16 originals
+    (binary16 ingest) and at most 4 q-heads per KV head; any other geometry --
+    including the reference's own defaults (head_dim=64, float32 ingest) --
+    raises ValueError instead of being coerced.
+    """
     kind: str = "gaussian"
     n_tokens: int = 1024
-    head_dim: int = 128
+    head_dim: int = 64
     block_size: int = 16
     group_size: int = 16
-    query_heads: int = 4
+    query_heads: int = 1
     kv_heads: int = 1
     steps: int = 8
     seed: int = 0
-    ingest_binary16: bool = True
+    ingest_binary16: bool = False
 
     def __post_init__(self):
         if self.kind not in WORKLOAD_KINDS:
@@ -46,6 +53,15 @@ class WorkloadConfig:
             raise ValueError("kv_heads must divide query_heads")
         if self.head_dim % self.group_size != 0:
             raise ValueError("group_size must divide head_dim")
+        if (self.head_dim, self.block_size, self.group_size) != (_lib.HEAD_DIM, _lib.BLOCK,
+                                                                 _lib.GROUP):
+            raise ValueError("the device path supports head_dim=128, block_size=16, "
+                             f"group_size=16 (got {self.head_dim}, {self.block_size}, "
+                             f"{self.group_size})")
+        if not self.ingest_binary16:
+            raise ValueError("the device path stores FP16 originals: ingest_binary16 must be True")
+        if self.query_heads // self.kv_heads > _lib.MAX_QHEADS:
+            raise ValueError("the device path supports up to 4 query heads per KV head")
 
     @property
     def group_factor(self):

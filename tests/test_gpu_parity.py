@@ -237,7 +237,7 @@ def test_fault_injection_trips_canary(ck):
     keys = keys.astype(np.float16).astype(np.float64)
     vals = vals.astype(np.float16).astype(np.float64)
     q = 3.0 * w + rng.standard_normal(128)
-    cache = ck.TieredCache(16, 128, 16, max_tokens=128)
+    cache = ck.TieredCache(16, 128, 16, ingest_binary16=True, max_tokens=128)
     cache.append_tokens(keys, vals)
     kv = oracle.OracleKV(16, 128, 16, ingest_binary16=True, narrow=True)
     kv.append_tokens(keys, vals)
@@ -259,7 +259,7 @@ def test_fault_injection_trips_canary(ck):
 
 def test_tier2_loss_is_hard_error(ck):
     rng = np.random.default_rng(5)
-    cache = ck.TieredCache(16, 128, 16, max_tokens=256)
+    cache = ck.TieredCache(16, 128, 16, ingest_binary16=True, max_tokens=256)
     cache.append_tokens(rng.standard_normal((100, 128)), rng.standard_normal((100, 128)))
     cache.dev.drop_tier2(0, 0)
     with pytest.raises(ck.Tier2UnavailableError):
@@ -267,7 +267,7 @@ def test_tier2_loss_is_hard_error(ck):
 
 
 def test_empty_cache_raises(ck):
-    cache = ck.TieredCache(16, 128, 16, max_tokens=64)
+    cache = ck.TieredCache(16, 128, 16, ingest_binary16=True, max_tokens=64)
     with pytest.raises(ck.EmptyCacheError):
         ck.run_decode_step(np.zeros(128), cache, ck.PolicyConfig(exploration_rate=0.0))
 
@@ -275,7 +275,7 @@ def test_empty_cache_raises(ck):
 def test_partial_only_cache(ck):
     rng = np.random.default_rng(6)
     k, v = rng.standard_normal((9, 128)), rng.standard_normal((9, 128))
-    cache = ck.TieredCache(16, 128, 16, max_tokens=64)
+    cache = ck.TieredCache(16, 128, 16, ingest_binary16=True, max_tokens=64)
     cache.append_tokens(k, v)
     q = rng.standard_normal(128)
     a = ck.run_decode_step(q, cache, ck.PolicyConfig(exploration_rate=0.0))
@@ -320,7 +320,7 @@ def test_host_tier2_matches_device_tier2(ck, monkeypatch, env):
     by the separate gather kernel) gives the same step as Tier-2 in HBM."""
     for key, val in env.items():
         monkeypatch.setenv(key, val)
-    cfg = ck.WorkloadConfig(kind="sink", n_tokens=3000, head_dim=128, query_heads=8, kv_heads=2,
+    cfg = ck.WorkloadConfig(ingest_binary16=True, kind="sink", n_tokens=3000, head_dim=128, query_heads=8, kv_heads=2,
                             steps=4, seed=4)
     pol = ck.PolicyConfig(exploration_rate=0.0, v_tol=0.01)
     outs = []

@@ -59,7 +59,7 @@ def test_storage_table_matches_oracle():
 
 def test_synth_arrays_match_oracle_generator():
     for kind in ("gaussian", "sink", "needle", "near_tie"):
-        cfg = WorkloadConfig(kind=kind, n_tokens=100, head_dim=128, query_heads=8, kv_heads=2,
+        cfg = WorkloadConfig(ingest_binary16=True, kind=kind, n_tokens=100, head_dim=128, query_heads=8, kv_heads=2,
                              steps=3, seed=4)
         k, v, q = synth_arrays(cfg)
         o = make_workload(kind=kind, n_tokens=100, head_dim=128, query_heads=8, kv_heads=2,
@@ -71,7 +71,7 @@ def test_synth_arrays_match_oracle_generator():
 def test_telemetry_schema_matches_oracle():
     """A device-shaped record built from certificates aggregates exactly like
     the oracle's (harness.py:397-499)."""
-    cfg = WorkloadConfig(kind="gaussian", n_tokens=64, head_dim=128, query_heads=4,
+    cfg = WorkloadConfig(ingest_binary16=True, kind="gaussian", n_tokens=64, head_dim=128, query_heads=4,
                          kv_heads=1, steps=2)
     recs = []
     for s in range(2):
@@ -88,3 +88,46 @@ def test_telemetry_schema_matches_oracle():
     b = oracle_aggregate(recs, 4)
     assert a == b
     assert a["rates"]["dense_fraction"] == 0.25
+
+
+# ---- boundary fidelity: unsupported reference geometry is refused, not coerced ----
+
+def test_workload_config_rejects_unsupported_geometry():
+    with pytest.raises(ValueError, match="head_dim=128"):
+        WorkloadConfig()  # the reference defaults: head_dim 64, float32 ingest
+    with pytest.raises(ValueError, match="ingest_binary16"):
+        WorkloadConfig(head_dim=128)
+    with pytest.raises(ValueError, match="group_size"):
+        WorkloadConfig(head_dim=128, group_size=32, ingest_binary16=True)
+    with pytest.raises(ValueError, match="4 query heads"):
+        WorkloadConfig(head_dim=128, ingest_binary16=True, query_heads=8, kv_heads=1)
+    cfg = WorkloadConfig(head_dim=128, ingest_binary16=True, query_heads=4)
+    assert WorkloadConfig.from_dict(cfg.to_dict()) == cfg
+    # field names and the remaining defaults are the reference's (harness.py:41-51)
+    assert (cfg.kind, cfg.n_tokens, cfg.block_size, cfg.kv_heads, cfg.steps, cfg.seed) == \
+        ("gaussian", 1024, 16, 1, 8, 0)
+
+
+def test_tiered_cache_rejects_float32_ingest_and_other_dims():
+    from paper_2605_20868_b200 import TieredCache
+    with pytest.raises(ValueError, match="ingest_binary16"):
+        TieredCache(16, 128, 16)  # reference default ingest_binary16=False (cache.py:52)
+    with pytest.raises(ValueError, match="ingest_binary16"):
+        TieredCache(16, 128, 16, ingest_binary16=False)
+    with pytest.raises(ValueError, match="head_dim=128"):
+        TieredCache(16, 64, 16, ingest_binary16=True)
+    with pytest.raises(ValueError, match="does not divide"):
+        TieredCache(16, 128, 48, ingest_binary16=True)
+
+
+def test_scratch_cache_reference_view_and_page_report():
+    from paper_2605_20868_b200 import ScratchCache
+    from paper_2605_20868_b200.cache import PageInReport
+    with pytest.raises(ValueError):
+        ScratchCache(-1)
+    s = ScratchCache(8)
+    assert (s.hits, s.misses, s.bytes_paged_in, s.hit_rate) == (0, 0, 0, 0.0)
+    s._account(3, 1, 4096)
+    assert (s.hits, s.misses, s.bytes_paged_in, s.hit_rate) == (3, 1, 4096, 0.75)
+    r = PageInReport(2, 1, 4096)
+    assert r.to_dict() == {"hits": 2, "misses": 1, "bytes": 4096} and r.payloads == {}
