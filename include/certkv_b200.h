@@ -83,6 +83,8 @@ typedef struct {
  * sticky; TIER2 is per decode step (cleared when the step begins, set by any
  * kernel of the step that needed a lost Tier-2 block); APPEND_BAD is the
  * verdict of the append in flight (cleared when it begins). */
+#define CKV_MAX_BLOCKS 32768 /* full blocks per unit the selection holds (524288 tokens) */
+
 #define CKV_ST_NONFINITE 0
 #define CKV_ST_CAPACITY 1
 #define CKV_ST_TIER2 2

@@ -383,7 +383,7 @@ def decode_step(q, kv, policy, key_scratch=None, value_scratch=None,
         "promoted": promoted, "value_promotions": vprom, "order": dec["order"],
         "masses": dec["masses"], "partial_mass": dec["partial_mass"],
         "log_mass_p1": p1["log_mass"], "log_mass_p2": att["log_mass"],
-        "block_masses_p2": att["block_masses"], "pages": pages,
+        "block_masses_p2": att["block_masses"], "etas": kv.etas(), "pages": pages,
         "head": head, "step": step,
     }
 

@@ -115,7 +115,7 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
                     ckv_step* st) {
   if (!pol || !st || n_units <= 0 || max_blocks <= 0 || n_heads < 1 || n_heads > CKV_MAX_QHEADS)
     return CKV_EINVAL;
-  if (max_blocks > 256 * 128) return CKV_EINVAL;  /* selection holds <= 32768 blocks per unit */
+  if (max_blocks > CKV_MAX_BLOCKS) return CKV_EINVAL;  /* selection holds <= 32768 blocks per unit */
   if (pol->k_max < 0 || pol->k_min < 0 || pol->k_max < pol->k_min || pol->k_max > 511 ||
       pol->ranking_depth < 1 || pol->ranking_depth > 64)
     return CKV_EINVAL;

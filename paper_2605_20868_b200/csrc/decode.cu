@@ -516,6 +516,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
   const double lse = (double)lmax + log(se);
   const float lsef = (float)lse;
   const double pmass = (pl > 0) ? exp((double)lmp - lse) : 0.0;
+  // the reference orders fp64 masses exp(l' - lse) (attention.py:183): masses that
+  // underflow to exactly 0 there (l' - lse < -745.13) tie and keep block order, so
+  // the selection gives all of them one key just below every other key
+  const uint32_t zk = okey((float)(lse - 745.1332191019412));
+  auto skey = [&](int j) -> uint32_t { return kk[j] < zk ? zk - 1u : kk[j]; };
 
   SELPROF(4);
   // ---- top K_sel blocks by l' (ties -> lower index) -------------------------------
@@ -538,8 +543,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       if (BJ(j) < nb) {
-        kmn = min(kmn, kk[j]);
-        kmx = max(kmx, kk[j]);
+        kmn = min(kmn, skey(j));
+        kmx = max(kmx, skey(j));
       }
     }
     kmn = __reduce_min_sync(0xffffffffu, kmn);
@@ -570,7 +575,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
-        const uint32_t rel = kk[j] - kmn;
+        const uint32_t rel = skey(j) - kmn;
         const bool in = BJ(j) < nb && (rel & pmask) == prefix;
         if (in) atomicAdd(&S.hist[(rel >> shift) & (uint32_t)(nbins - 1)], 1);
       }
@@ -615,13 +620,13 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
       // candidates: every key >= T (the lower edge of the last bin), block order
       int nc = 0;
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) nc += (BJ(j) < nb && kk[j] >= T);
+      for (int j = 0; j < KPT; ++j) nc += (BJ(j) < nb && skey(j) >= T);
       int pc = block_excl_scan(nc, S.wsum, &S.misc[3]);
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
         const int b = BJ(j);
-        if (b < nb && kk[j] >= T)
-          S.cand[pc++] = ((unsigned long long)kk[j] << 32) |
+        if (b < nb && skey(j) >= T)
+          S.cand[pc++] = ((unsigned long long)skey(j) << 32) |
                          (unsigned long long)(0xffffffffu - (uint32_t)b);
       }
       n_sorted = n_cand;
@@ -630,23 +635,23 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
       // in block order; blocks run j-major (BJ), so one scan per j (rare path)
       int ngt = 0;
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) ngt += (kk[j] > T);
+      for (int j = 0; j < KPT; ++j) ngt += (BJ(j) < nb && skey(j) > T);
       int pg = block_excl_scan(ngt, S.wsum, &S.misc[2]);
       const int tot_gt = S.misc[2];
 #pragma unroll
       for (int j = 0; j < KPT; ++j)
-        if (kk[j] > T)
-          S.cand[pg++] = ((unsigned long long)kk[j] << 32) |
+        if (BJ(j) < nb && skey(j) > T)
+          S.cand[pg++] = ((unsigned long long)skey(j) << 32) |
                          (unsigned long long)(0xffffffffu - (uint32_t)BJ(j));
       int taken = tot_gt;
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
         if (taken >= ksel) continue;  // uniform across the block
-        const bool eq = BJ(j) < nb && kk[j] == T;
+        const bool eq = BJ(j) < nb && skey(j) == T;
         const int pos = taken + block_excl_scan((int)eq, S.wsum, &S.misc[3]);
         const int cnt = S.misc[3];
         if (eq && pos < ksel)
-          S.cand[pos] = ((unsigned long long)kk[j] << 32) |
+          S.cand[pos] = ((unsigned long long)skey(j) << 32) |
                         (unsigned long long)(0xffffffffu - (uint32_t)BJ(j));
         taken += cnt;
       }

@@ -644,6 +644,58 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
     }
   }
 
+  // E_val's terms are taken relative to the Phase-1 lse.  When Phase 2 moves every
+  // mass more than ~700 nats below it (corrupted key metadata: the canary trips by
+  // orders of magnitude) they underflow in fp64; then E_val is recomputed from the
+  // block log-masses against the Phase-2 maximum (certifier.py:153-160) -- one
+  // pass over the unit's blocks, on this rare path only
+  __shared__ double ev_fix;
+  if (!(hs.alpha_hat + hs.partial_mass + sF > 1e-250)) {
+    __shared__ uint32_t fb[(CKV_MAX_BLOCKS + 31) / 32], vb[(CKV_MAX_BLOCKS + 31) / 32];
+    __shared__ float mw[4];
+    __shared__ double nw[4], dw[4];
+    const int nb = c.n_blocks[u];
+    const int nw32 = (nb + 31) / 32;
+    for (int i = tid; i < nw32; i += blockDim.x) fb[i] = vb[i] = 0u;
+    __syncthreads();
+    const int32_t* vl = st.vlist + hu * c.max_blocks;
+    for (int i = tid; i < kp; i += blockDim.x) atomicOr(&fb[order[i] >> 5], 1u << (order[i] & 31));
+    for (int i = tid; i < hs.n_v; i += blockDim.x) atomicOr(&vb[vl[i] >> 5], 1u << (vl[i] & 31));
+    __syncthreads();
+    const float* lm1 = st.lm1 + hu * c.max_blocks;
+    auto ell = [&](int b) -> float { return ((fb[b >> 5] >> (b & 31)) & 1u) ? lm2[b] : lm1[b]; };
+    const float lpart = (pl > 0) ? hs.mp + logf(hs.lp) : ninf();
+    float mx = lpart;
+    for (int b = tid; b < nb; b += blockDim.x) mx = fmaxf(mx, ell(b));
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) mw[tid >> 5] = mx;
+    __syncthreads();
+    mx = fmaxf(fmaxf(mw[0], mw[1]), fmaxf(mw[2], mw[3]));
+    double num = 0.0, den = 0.0;
+    const float* eta = c.eta + (size_t)u * c.max_blocks;
+    for (int b = tid; b < nb; b += blockDim.x) {
+      const double w = exp((double)ell(b) - (double)mx);
+      den += w;
+      if (!((vb[b >> 5] >> (b & 31)) & 1u)) num += w * (double)eta[b];
+    }
+    num = warp_sum_d(num);
+    den = warp_sum_d(den);
+    if ((tid & 31) == 0) {
+      nw[tid >> 5] = num;
+      dw[tid >> 5] = den;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      num = (nw[0] + nw[1]) + (nw[2] + nw[3]);
+      den = (dw[0] + dw[1]) + (dw[2] + dw[3]);
+      if (pl > 0) den += exp((double)lpart - (double)mx);
+      ev_fix = (den > 0.0) ? num / den : 0.0;
+    }
+    __syncthreads();
+  } else if (tid == 0) {
+    ev_fix = -1.0;
+  }
+
   if (tid == 0) {
     ckv_cert& ct = st.cert[hu];
     uint32_t fl = ct.flags;
@@ -669,7 +721,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
     // certifier.py:191-212 records both exponent modes; returned_e_key uses mode 3
     ct.e_key_tight = 2.0 * vmax * exp(2.0 * delta) * at * (exp(2.0 * delta) - 1.0);
     ct.e_key_impl = 2.0 * vmax * exp(3.0 * delta) * at * (exp(2.0 * delta) - 1.0);
-    ct.e_val = (denomE > 0.0) ? (hs.e_tail + eF) / denomE : 0.0;
+    ct.e_val = (ev_fix >= 0.0) ? ev_fix : (hs.e_tail + eF) / denomE;
     ct.canary_gap = (double)canary;
     ct.flags = fl;
     int kind = 0;

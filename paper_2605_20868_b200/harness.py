@@ -239,8 +239,12 @@ def _scr(h, m):
 
 
 def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layers=1,
-                 keep_outputs=False):
-    """Drive a workload through decode (harness.py:339-394)."""
+                 keep_outputs=False, keep_decisions=False):
+    """Drive a workload through decode (harness.py:339-394).
+
+    ``keep_outputs`` adds ``result.outputs`` (per step, [query_heads, d]);
+    ``keep_decisions`` adds ``result.decisions`` (per step, per q-head: the
+    promoted block ids and the value-promoted block ids, ascending)."""
     cfg = workload.config
     if cfg.group_factor > _lib.MAX_QHEADS:
         raise ValueError("device path supports up to 4 query heads per KV head")
@@ -249,7 +253,7 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
     scratch = ScratchCache(key_capacity, value_capacity)
     dec = CertifiedDecoder(cache, policy, n_heads=cfg.group_factor, scratch=scratch)
     gf = cfg.group_factor
-    records, outputs = [], []
+    records, outputs, decisions = [], [], []
     for step in range(cfg.steps):
         q = torch.from_numpy(workload.queries[step].reshape(cfg.kv_heads, gf, cfg.head_dim))
         res = dec.step(q.to(cache.device), rng=explore_rng)
@@ -274,6 +278,10 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
                                    bytes_paged, res.staging_bytes, fr))
         if keep_outputs:
             outputs.append(res.out.double().cpu().numpy().reshape(cfg.query_heads, -1).copy())
+        if keep_decisions:
+            decisions.append([(sorted(int(b) for b in res.promoted(*divmod(h, gf))),
+                               sorted(int(b) for b in res.value_promotions(*divmod(h, gf))))
+                              for h in range(cfg.query_heads)])
         cache.append(torch.from_numpy(workload.new_keys[step])[:, None, :],
                      torch.from_numpy(workload.new_values[step])[:, None, :])
     header = {"config": cfg.to_dict(), "policy": policy.to_dict(), "seed": cfg.seed,
@@ -283,6 +291,8 @@ def run_workload(workload, policy, key_capacity=2048, value_capacity=2048, layer
     rr = RunResult(header, records, aggregate_telemetry(records, cfg, layers=layers))
     if keep_outputs:
         rr.outputs = outputs
+    if keep_decisions:
+        rr.decisions = decisions
     return rr
 
 

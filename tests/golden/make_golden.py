@@ -22,6 +22,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(1, os.path.dirname(os.path.dirname(HERE)))  # the repo root (oracle.margins)
 os.environ["CERTKV_KERNEL"] = "pure"
 
 import certkv  # noqa: E402
@@ -94,7 +95,44 @@ RUNS = [
                         kv_heads=2, steps=2, seed=11), dict(exploration_rate=0.0, v_tol=0.01), (2048, 2048)),
     ("d64", dict(kind="gaussian", n_tokens=333, head_dim=64, query_heads=4,
                  kv_heads=2, steps=2, seed=9), dict(exploration_rate=0.0, k_max=4), (8, 8)),
+    # BASELINE.json C1 exactly: the reference's own CPU-runnable case
+    ("c1", dict(kind="gaussian", n_tokens=4096, head_dim=128, query_heads=32, kv_heads=8,
+                steps=16, seed=0), dict(exploration_rate=0.0), (2048, 2048)),
+    # decisions away from "everything promoted": a real K* cut, value promotions
+    # with an evicting scratch, greedy Rung 2
+    ("gauss16k", dict(kind="gaussian", n_tokens=16384, head_dim=128, query_heads=4,
+                      kv_heads=1, steps=3, seed=12), dict(exploration_rate=0.0), (2048, 2048)),
+    ("sink8k_vtol", dict(kind="sink", n_tokens=8192, head_dim=128, query_heads=8, kv_heads=2,
+                         steps=3, seed=13), dict(exploration_rate=0.0, v_tol=0.002), (512, 256)),
+    ("greedy", dict(kind="sink", n_tokens=2000, head_dim=128, query_heads=4, kv_heads=1,
+                    steps=2, seed=14), dict(exploration_rate=0.0, greedy_value_budget=0.05),
+     (2048, 2048)),
 ]
+
+# runs whose outputs are frozen as float32 (size; the tests compare at >= 1e-6)
+F32_OUTPUTS = {"c1"}
+
+
+def _margins(r, phase1, cache, policy):
+    """Threshold distances of the reference's own decisions (oracle/margins.py),
+    computed from the reference objects of this head-step."""
+    from oracle.margins import as_row, decision_margins
+    dec, att = r.decision, r.attend
+    F = sorted(dec.promoted)
+    gap = 0.0
+    if F:
+        bs = cache.block_size
+        idx = np.concatenate([np.arange(b * bs, (b + 1) * bs) for b in F])
+        gap = float(np.abs(att.token_scores[idx] - phase1.token_scores[idx]).max())
+    m = decision_margins(
+        dec.normalized_masses, dec.order, dec.k_star, dec.k_coverage, dec.partial_mass,
+        cache.etas(), phase1.log_mass, dict(att.promoted_log_masses), r.delta_h, gap,
+        tau_cov=policy.tau_cov, k_min=policy.k_min, k_max=policy.k_max, v_tol=policy.v_tol,
+        greedy_value_budget=policy.greedy_value_budget, ranking_depth=policy.ranking_depth,
+        epsilon_guard=policy.epsilon_guard, rung2_enabled=policy.rung2_enabled,
+        ranking_checks_enabled=policy.ranking_checks_enabled,
+        canary_enabled=policy.canary_enabled)
+    return as_row(m)
 
 
 def _digest(arr):
@@ -122,8 +160,9 @@ def workload_golden():
                      c["rung_flags"]["rung1"], c["rung_flags"]["rung2"],
                      c["rung_flags"]["rung3"], c["rung_flags"]["rung4"]])
         # per head-step outputs and promoted sets via a replay with hooks
-        outs, prom, vprom = [], [], []
+        outs, prom, vprom, margins = [], [], [], []
         wl2 = generate_workload(cfg)
+        from certkv.attention import phase1_score
         from certkv.cache import ScratchCache
         from certkv.harness import run_decode_step, _rng
         ks = [ScratchCache(kc) for _ in wl2.caches]
@@ -136,6 +175,8 @@ def workload_golden():
                 r = run_decode_step(wl2.queries[step, h], wl2.caches[kv], policy,
                                     ks[kv], vs[kv], rng, h, step)
                 step_res.append(r)
+                margins.append(_margins(r, phase1_score(wl2.queries[step, h], wl2.caches[kv]),
+                                        wl2.caches[kv], policy))
                 prom.append(sorted(r.decision.promoted))
                 vprom.append(sorted(r.value_promotions))
             if any(r.rung4_requested for r in step_res):
@@ -158,7 +199,8 @@ def workload_golden():
         np.savez_compressed(
             os.path.join(HERE, f"run_{name}.npz"),
             cert=np.asarray(arrays["cert"], dtype=np.float64),
-            outputs=np.asarray(outs), promoted=pm, value_promotions=vm,
+            outputs=np.asarray(outs, dtype=np.float32 if name in F32_OUTPUTS else np.float64),
+            margins=np.asarray(margins, dtype=np.float64), promoted=pm, value_promotions=vm,
             records_json=np.asarray(recs), summary_json=np.asarray(summ))
         manifest[name] = {"workload": wkw, "policy": pkw, "capacities": [kc, vc],
                           "keys_digest": keys_digest, "queries_digest": q_digest}

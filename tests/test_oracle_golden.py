@@ -14,6 +14,7 @@ import pytest
 
 import oracle
 from oracle import quant
+from oracle.margins import as_row, margins_from_oracle
 from oracle.step import OraclePolicy, make_workload, run_workload
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -85,7 +86,8 @@ def test_run_workload_golden(name):
     assert hashlib.sha256(np.ascontiguousarray(keys).tobytes()).hexdigest() == spec["keys_digest"]
     assert hashlib.sha256(wl["queries"].tobytes()).hexdigest() == spec["queries_digest"]
     kc, vc = spec["capacities"]
-    res = run_workload(wl, OraclePolicy(**spec["policy"]), kc, vc)
+    pol = OraclePolicy(**spec["policy"])
+    res = run_workload(wl, pol, kc, vc)
     z = _load(f"run_{name}.npz")
     recs = json.loads(str(z["records_json"]))
     summ = json.loads(str(z["summary_json"]))
@@ -105,6 +107,12 @@ def test_run_workload_golden(name):
             assert r["promoted"].tolist() == p[p >= 0].tolist()
             v = z["value_promotions"][i]
             assert r["value_promotions"].tolist() == v[v >= 0].tolist()
+            # threshold distances of every decision, as the reference's own objects give them
+            m = np.asarray(as_row(margins_from_oracle(r, pol)))
+            g = z["margins"][i]
+            assert np.array_equal(np.isinf(m), np.isinf(g)), (i, m, g)
+            fin = ~np.isinf(g)
+            np.testing.assert_allclose(m[fin], g[fin], rtol=1e-6, atol=1e-12)
             i += 1
         for key in ("rung_counts", "cause_counts", "key_scratch", "value_scratch",
                     "bytes_paged_in", "rung4_staging_bytes", "k_star_mean"):
