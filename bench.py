@@ -10,8 +10,10 @@ ranks all-gather outputs + certificates over NCCL.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints one JSON line (rank 0).  `--impl reference` times the CPU oracle port
-of the reference path (oracle/, NumPy) on the host cores instead.
+Prints one JSON line (rank 0).  `--impl reference` times the reference's own
+CPU implementation on the host cores instead: the unmodified certkv package
+with its compiled kernel backend, built into oracle/_ref by oracle/build_ref.sh
+(the oracle/ NumPy port only if that build is missing).
 """
 
 import argparse
@@ -38,6 +40,13 @@ PRESETS = {
     "c3": dict(ctx=131072, batch=1, tier2="device", scratch=-1, v_tol=None, adversarial=False,
                desc="C3: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, 131072 ctx, batch 1, "
                     "KV-head sharded"),
+    # the north-star placement of C3: Tier-2 originals in pinned host RAM, the
+    # reference's default 2048-block scratch per KV head (harness.py:339), misses
+    # paged in over PCIe
+    "c3host": dict(ctx=131072, batch=1, tier2="host", scratch=2048, v_tol=None, adversarial=False,
+                   desc="C3 with Tier-2 in pinned host RAM: Llama-3.1-8B attention, 32 layers x "
+                        "GQA 32/8, d=128, 131072 ctx, batch 1, 2048-block LRU scratch per KV head "
+                        "in HBM, misses paged in over PCIe"),
     "c4": dict(ctx=16384, batch=32, tier2="host", scratch=-1, v_tol=1e-3, adversarial=False,
                desc="C4: Llama-3.1-8B attention, 32 layers x GQA 32/8, d=128, 16384 ctx, batch 32, "
                     "tight v_tol (value promotions), Tier-2 in pinned host RAM (page-in)"),
@@ -167,7 +176,8 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------
-# CPU oracle timing (reference arm and cpu_baseline)
+# CPU arm: the unmodified reference (oracle/_ref, built by oracle/build_ref.sh)
+# or, if that build is absent, the oracle port
 # -------------------------------------------------------------------------
 
 _W = {}
@@ -188,7 +198,7 @@ def _worker_init(ctx, seed, n_heads):
 
 
 def _worker_step(_):
-    """One unit-step of the reference path: n_heads certified q-heads, then
+    """One unit-step of the oracle port: n_heads certified q-heads, then
     quantize-on-append of the new token (harness.py:351-382)."""
     import oracle
     from oracle.step import OraclePolicy
@@ -201,25 +211,36 @@ def _worker_step(_):
     return time.perf_counter() - t0
 
 
-def cpu_reference(args, total_units, steps, warmup, workers):
-    """Time the oracle port on `workers` host processes; each step runs one
-    unit-step per worker and is scaled to the full step (total_units)."""
+def _port_reference(args, total_units, steps, warmup, workers):
     import multiprocessing as mp
     ctx = mp.get_context("fork")
-    t_build = time.perf_counter()
     with ctx.Pool(workers, initializer=_worker_init,
                   initargs=(args.ctx, 1234, args.q_per_kv)) as pool:
-        pool.map(_worker_step, range(workers))  # make every worker build its cache
-        build_s = time.perf_counter() - t_build
+        pool.map(_worker_step, range(workers))
         for _ in range(warmup):
             pool.map(_worker_step, range(workers))
         t0 = time.perf_counter()
         for _ in range(steps):
             pool.map(_worker_step, range(workers))
         dt = (time.perf_counter() - t0) / steps
-    # one pool round = `workers` unit-steps; a full step needs total_units
-    sec_per_step = dt * total_units / workers
-    return 1.0 / sec_per_step, dt, build_s
+    return dt * total_units / workers
+
+
+def cpu_reference(args, total_units, steps, warmup, workers):
+    """Seconds per full decode step on `workers` host processes (one unit each,
+    single-threaded), scaled from `workers` unit-steps to `total_units`.
+    Returns (steps/s, kind, detail)."""
+    from oracle import ref_arm
+    if ref_arm.available():
+        r = ref_arm.time_reference(args.ctx, args.q_per_kv, total_units, steps, warmup, workers,
+                                   v_tol=args.v_tol, adversarial=args.adversarial)
+        return 1.0 / r["sec_per_step"], "reference", {
+            "impl": "unmodified certkv (oracle/_ref) harness.run_workload, kernel backend "
+                    f"'{r['backend']}'", "unit_step_s": r["round_s"], "prefill_s": r["prefill_s"],
+            "host": ref_arm.host_info()}
+    sec = _port_reference(args, total_units, steps, warmup, workers)
+    return 1.0 / sec, "port", {"impl": "oracle/ NumPy port (oracle/_ref not built)",
+                               "host": ref_arm.host_info()}
 
 
 # -------------------------------------------------------------------------
@@ -259,16 +280,18 @@ def main():
             ncpu = len(os.sched_getaffinity(0))
         except Exception:
             ncpu = os.cpu_count() or 1
-        workers = max(1, min(ncpu, 32))
-        rate, dt, build_s = cpu_reference(args, total_units, K, W, workers)
+        workers = max(1, min(ncpu, 32, total_units))
+        rate, kind, detail = cpu_reference(args, total_units, K, W, workers)
         line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
                 "warmup": W, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "impl": "reference",
-                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
-                                 "sample": f"{workers} of {total_units} units (one per process) "
-                                           f"at {args.ctx} ctx, {args.q_per_kv} q-heads each, "
-                                           f"per step; scaled x{total_units / workers:.1f}"},
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": kind,
+                                 "sample": f"{workers} of {total_units} units (one per process, "
+                                           f"single-threaded) at {args.ctx} ctx, {args.q_per_kv} "
+                                           f"q-heads each, {K} timed steps after {W} warm-up; "
+                                           f"scaled x{total_units / workers:.1f}",
+                                 **detail},
                 "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -516,20 +539,26 @@ def main():
     achieved = tier1_bytes_launch / (pa_ms / 1000.0) / 1e9
     step_bytes = total_units * args.ctx * 288.0
     step_frac = step_bytes / (ms / 1000.0) / 1e9 / peak
+    # DRAM bytes per pass-A launch from an ncu capture of THIS configuration
+    # (tools/traffic.py -> profiles/traffic_r02.json, keyed by the workload shape)
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "pass_a_traffic.json")
+    tkey = f"{args.config}:{args.ctx}:{args.batch}:{args.tier2}:{U}"
+    tfile = os.path.join(ROOT, "profiles", "traffic_r02.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get("bytes_per_launch")
+            ent = json.load(open(tfile)).get(tkey)
+            if ent:
+                traffic = ent["k_pass_a"]["dram_bytes_per_launch"]
         except Exception:
             traffic = None
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        rate, dt, _ = cpu_reference(args, total_units, 2, 1, 1)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+        rate, kind, detail = cpu_reference(args, total_units, 2, 1, 1)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
                "sample": f"1 of {total_units} units at {args.ctx} ctx ({args.q_per_kv} q-heads "
-                         f"+ append), 2 timed unit-steps on one core, scaled x{total_units}"}
+                         f"+ append), 2 timed unit-steps on one core, scaled x{total_units}",
+               **detail}
 
     value = 1000.0 / ms
     line = {

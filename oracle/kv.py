@@ -18,6 +18,14 @@ class PagingFault(RuntimeError):
     """Mirror of cache.PagingError (cache.py:37-39)."""
 
 
+def _f32_up(x):
+    """float32 rounded toward +inf, as a Python float (the device's annotation width)."""
+    f = np.float32(x)
+    if float(f) < x:
+        f = np.nextafter(f, np.float32(np.inf))
+    return float(f)
+
+
 class OracleKV:
     """Block-organised store for one KV head (cache.py:49-224).
 
@@ -80,6 +88,8 @@ class OracleKV:
         us, uo = self.value_meta(vs, vo)
         eta, nu = quant.value_annotations(
             v32, quant.dequant_values(vc, us, uo, self.group_size))
+        if self.narrow:  # the device stores them as float32 rounded up
+            eta, nu = _f32_up(eta), _f32_up(nu)
         self.kcodes.append(kc); self.kscale.append(ks); self.koffset.append(ko)
         self.vcodes.append(vc); self.vscale.append(vs); self.voffset.append(vo)
         self.eta.append(eta); self.nu.append(nu)

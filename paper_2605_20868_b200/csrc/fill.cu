@@ -189,11 +189,13 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
     }
     if (tid == 0) {
       size_t ib = (size_t)u * c.max_blocks + b;
-      c.eta[ib] = (float)e;
-      c.nu[ib] = (float)n;
+      // rounded up to fp32: E_val / E_key built from the stored annotations stay
+      // upper bounds of the fp64 ones (certifier.py:135-160)
+      c.eta[ib] = __double2float_ru(e);
+      c.nu[ib] = __double2float_ru(n);
       c.kscale_max[ib] = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
       c.tier2_valid[ib] = 1;
-      atomicMax(reinterpret_cast<int*>(&c.v_max[u]), __float_as_int((float)n));
+      atomicMax(reinterpret_cast<int*>(&c.v_max[u]), __float_as_int(__double2float_ru(n)));
     }
   }
   // ---- write the record -------------------------------------------------------

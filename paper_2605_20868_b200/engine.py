@@ -420,3 +420,27 @@ def dense_attention(query, cache):
     s = (k.double() @ q) / np.sqrt(D)
     w = torch.softmax(s, 0)
     return (w @ v.double()).cpu().numpy()
+
+
+# -- the dense rungs as standalone calls (fallback.py:230-255) ----------------
+
+
+def rung3_per_head(query, cache):
+    """Dense recomputation of one head: the exact routine (dense_attention)."""
+    return dense_attention(query, cache)
+
+
+def rung4_staging_bytes(token_counts, head_dim):
+    """FP16 K and V staged for an all-head dense recomputation: 2 * N * d * 2
+    bytes per distinct cache (fallback.py:235-238)."""
+    return int(sum(2 * int(n) * int(head_dim) * 2 for n in token_counts))
+
+
+def rung4_all_heads(queries, caches):
+    """Dense outputs for every query head (one cache per head, grouped heads
+    repeat their cache) and the staging bytes, charged once per distinct cache."""
+    if len(queries) != len(caches):
+        raise ValueError("need one cache reference per query head")
+    outs = [dense_attention(q, c) for q, c in zip(queries, caches)]
+    distinct = list({id(c): c for c in caches}.values())
+    return outs, rung4_staging_bytes([c.num_tokens for c in distinct], distinct[0].head_dim)

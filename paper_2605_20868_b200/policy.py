@@ -178,3 +178,13 @@ def events_from_flags(flags, head, step):
     if flags & _lib.F_NUMERIC:
         ev.append(FallbackEvent(4, head, step, CAUSE_PRECONDITION))
     return ev
+
+
+def e_key_bound(v_max, delta, est_tail_mass, exponent_mode):
+    """E_key = 2 v_max e^{e Delta} alpha_T (e^{2 Delta} - 1), e in {2, 3}
+    (certifier.py:135-144) -- the formula k_combine evaluates in fp64."""
+    if exponent_mode not in (2, 3):
+        raise ValueError("exponent_mode must be 2 or 3")
+    import math
+    return (2.0 * float(v_max) * math.exp(exponent_mode * float(delta)) * float(est_tail_mass)
+            * (math.exp(2.0 * float(delta)) - 1.0))
