@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--v-tol", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variant", action="store_true",
+                    help="skip the c3host variant measured after the default c3 line")
     args = ap.parse_args()
     pre = PRESETS[args.config]
     for k in ("ctx", "batch", "tier2", "scratch", "v_tol"):
@@ -247,70 +249,14 @@ def cpu_reference(args, total_units, steps, warmup, workers):
 # our arm
 # -------------------------------------------------------------------------
 
-def main():
-    args = parse()
+def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_wanted=True,
+            clocks_wanted=True):
+    """Build the cache of this rank's units, warm up, time K certified steps (CUDA
+    events, max over ranks), then the end-to-end loop through the public API.
+    Returns the measurements and the live objects (cache, decoder, scratch)."""
     import numpy as np
     import torch
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # test knob for exercising the sharded path on a single GPU (every rank on cuda:0, gloo)
-    if os.environ.get("CKV_BENCH_ONE_DEVICE"):
-        local = 0
-    K, W = args.steps, max(3, args.warmup)
-    total_units = args.layers * args.kv_heads * args.batch
-    pol_desc = "PolicyConfig(exploration_rate=0.0) defaults"
-    if args.v_tol is not None:
-        pol_desc = f"PolicyConfig(exploration_rate=0.0, v_tol={args.v_tol})"
-    tier1_gb = total_units * args.ctx * 288 / 1e9
-    config = {"workload": args.desc if args.ctx == PRESETS[args.config]["ctx"] else
-              f"{args.config.upper()} shape at {args.ctx} ctx, batch {args.batch}",
-              "ctx": args.ctx, "layers": args.layers, "kv_heads": args.kv_heads,
-              "q_heads": args.kv_heads * args.q_per_kv, "batch": args.batch,
-              "parallelism": f"kv-head shard x{args.gpus}",
-              "policy": pol_desc,
-              "l2": f"inputs larger than L2 (Tier-1 {tier1_gb:.2f} GB/step)",
-              "tier2": args.tier2}
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        try:
-            ncpu = len(os.sched_getaffinity(0))
-        except Exception:
-            ncpu = os.cpu_count() or 1
-        workers = max(1, min(ncpu, 32, total_units))
-        rate, kind, detail = cpu_reference(args, total_units, K, W, workers)
-        line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
-                "warmup": W, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config, "impl": "reference",
-                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": kind,
-                                 "sample": f"{workers} of {total_units} units (one per process, "
-                                           f"single-threaded) at {args.ctx} ctx, {args.q_per_kv} "
-                                           f"q-heads each, {K} timed steps after {W} warm-up; "
-                                           f"scaled x{total_units / workers:.1f}",
-                                 **detail},
-                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
-
-    import torch.distributed as dist
-    if world > 1:
-        torch.cuda.set_device(local)
-        if os.environ.get("CKV_BENCH_ONE_DEVICE"):
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import __graft_entry__
-    __graft_entry__.build()
-    import paper_2605_20868_b200 as ck
     from paper_2605_20868_b200 import _lib
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-
     # KV-head sharding: units are kv-major (sharding.unit_index); rank r owns whole KV heads
     if args.kv_heads % world:
         raise SystemExit("kv_heads must be divisible by the number of GPUs")
@@ -373,7 +319,7 @@ def main():
 
     launches = {"n": 0}
     dense_heads = {"n": 0}
-    stats = {"rung4": 0, "nv": 0.0, "pagein": 0, "steps": 0}
+    stats = {"rung4": 0, "nv": 0.0, "pagein": 0, "steps": 0, "hits": 0, "misses": 0}
     last = {}
     pending = {"p": None}
 
@@ -386,6 +332,8 @@ def main():
             stats["nv"] += float(res.cert["n_value_promoted"].mean())
             if res.page_stats is not None:
                 stats["pagein"] += int(res.page_stats[:, 1].sum() + res.page_stats[:, 3].sum()) * 4096
+                stats["hits"] += int(res.page_stats[:, 0].sum() + res.page_stats[:, 2].sum())
+                stats["misses"] += int(res.page_stats[:, 1].sum() + res.page_stats[:, 3].sum())
             stats["steps"] += 1
             last["res"] = res
             pending["p"] = None
@@ -412,14 +360,14 @@ def main():
     collect()
     if world > 1:
         dist.barrier()
-    sampler = ClockSampler(local, dev) if rank == 0 else None
+    sampler = ClockSampler(local, dev) if (rank == 0 and clocks_wanted) else None
     if sampler:
         sampler.start()
         if sampler.nv is None:
             time.sleep(0.3)  # nvidia-smi start-up
     launches["n"] = 0
     dense_heads["n"] = 0
-    stats.update(rung4=0, nv=0.0, pagein=0, steps=0)
+    stats.update(rung4=0, nv=0.0, pagein=0, steps=0, hits=0, misses=0)
     nb_timed = cache.num_blocks
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -445,7 +393,7 @@ def main():
 
     # ---- end to end through the public API with host buffers -----------------
     e2e = None
-    if not args.no_e2e:
+    if e2e_wanted:
         # steady state over E >= K steps (the one-step pipeline fill / drain amortised);
         # NP pinned input sets cycled
         E, NP = max(K, 40), min(max(K, 40), 8)
@@ -529,13 +477,170 @@ def main():
         e2e = {"value": 1000.0 / e_ms, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": E}
 
+    return dict(ms=ms, pa_ms=pa_ms, clocks=clocks, n_launch=n_launch, n_dense=n_dense,
+                stats=stats, last=last, dec=dec, cache=cache, scratch=scratch, e2e=e2e,
+                prefill_s=prefill_s, nb_timed=nb_timed, U=U, qpool=qpool)
+
+
+
+def _lru_ring(max_blocks, cap):
+    """Ring size of an LRU state (lru_ring in csrc/common.cuh)."""
+    if cap >= max_blocks:
+        return 0
+    need, r = 2 * cap + max_blocks + 1024, 1
+    while r < need:
+        r <<= 1
+    return r
+
+
+def pcie_peak_gbs(dev, nbytes=256 << 20):
+    """Pinned host -> HBM DMA bandwidth of this box (best of 3)."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = None
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        b.synchronize()
+        t = a.elapsed_time(b) / 1000.0
+        best = t if best is None else min(best, t)
+    return nbytes / best / 1e9
+
+
+def pcie_stats(args, R, ms):
+    """Host-Tier-2 configurations are PCIe-bound: bytes read from pinned host RAM
+    per step (misses paged into HBM slots by pass B + the dense rungs' blocks
+    that are not resident in a slot), the LRU hit rate of the timed steps, and the
+    achieved H2D rate against this box's measured DMA bandwidth."""
+    import numpy as np
+    import torch
+    dec, cache, sc, st = R["dec"], R["cache"], R["scratch"], R["stats"]
+    steps = max(1, st["steps"])
+    pagein = st["pagein"] / steps
+    dense_host, n = 0, 3
+    maxb = cache.max_blocks
+    for i in range(n):  # a few synchronous steps: slot tables as the dense kernel saw them
+        res = dec.step(R["qpool"][i])
+        units = np.nonzero((res.kinds != 0).any(1))[0]
+        nb = cache.num_blocks
+        for kind, lru, cap in ((0, sc.key_lru, sc.c.key_capacity), (1, sc.value_lru, sc.c.value_capacity)):
+            off = 4 + maxb + _lru_ring(maxb, cap)
+            for u in units:
+                resident = int((lru[int(u), off:off + nb] >= 0).sum()) if cap > 0 else 0
+                dense_host += (nb - resident) * 4096
+    dense_host /= n
+    total = pagein + dense_host
+    peak = pcie_peak_gbs(cache.device)
+    achieved = total / (ms / 1000.0) / 1e9
+    hm = st["hits"] + st["misses"]
+    return {"bound": "pcie", "pagein_bytes_per_step": pagein,
+            "dense_host_bytes_per_step": dense_host, "h2d_bytes_per_step": total,
+            "achieved_gbs": achieved, "peak_gbs_measured": peak, "frac": achieved / peak,
+            "scratch_hit_rate": st["hits"] / hm if hm else 0.0,
+            "scratch_blocks_per_kv_head": sc.c.key_capacity,
+            "note": "pinned-host Tier-2 read zero-copy by pass B (misses, filling their HBM "
+                    "slots) and by k_dense (dense rungs); peak = pinned DMA H2D of 256 MB"}
+
+
+def run_variant(args, ck, dev, dist, total_units, name="c3host", K=8, W=3):
+    """Another preset on the same box after the main line (fewer steps)."""
+    import copy
+    va = copy.copy(args)
+    pre = PRESETS[name]
+    for k in ("ctx", "batch", "tier2", "scratch", "v_tol"):
+        setattr(va, k, pre[k])
+    va.adversarial, va.desc, va.config = pre["adversarial"], pre["desc"], name
+    R = run_gpu(va, ck, dev, 1, 0, 0, K, W, dist, total_units, e2e_wanted=False,
+                clocks_wanted=False)
+    out = {"workload": pre["desc"], "value": 1000.0 / R["ms"], "unit": UNIT,
+           "ms_per_step": R["ms"], "steps": K, "warmup": W, "pass_a_ms": R["pa_ms"],
+           "hbm_frac_step": total_units * va.ctx * 288.0 / (R["ms"] / 1000.0) / 1e9 / peak_hbm()[0],
+           "dense_heads_in_timed_region": R["n_dense"]}
+    if va.tier2 == "host":
+        out["pcie"] = pcie_stats(va, R, R["ms"])
+    return out
+
+
+def main():
+    args = parse()
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test knob for exercising the sharded path on a single GPU (every rank on cuda:0, gloo)
+    if os.environ.get("CKV_BENCH_ONE_DEVICE"):
+        local = 0
+    K, W = args.steps, max(3, args.warmup)
+    total_units = args.layers * args.kv_heads * args.batch
+    pol_desc = "PolicyConfig(exploration_rate=0.0) defaults"
+    if args.v_tol is not None:
+        pol_desc = f"PolicyConfig(exploration_rate=0.0, v_tol={args.v_tol})"
+    tier1_gb = total_units * args.ctx * 288 / 1e9
+    config = {"workload": args.desc if args.ctx == PRESETS[args.config]["ctx"] else
+              f"{args.config.upper()} shape at {args.ctx} ctx, batch {args.batch}",
+              "ctx": args.ctx, "layers": args.layers, "kv_heads": args.kv_heads,
+              "q_heads": args.kv_heads * args.q_per_kv, "batch": args.batch,
+              "parallelism": f"kv-head shard x{args.gpus}",
+              "policy": pol_desc,
+              "l2": f"inputs larger than L2 (Tier-1 {tier1_gb:.2f} GB/step)",
+              "tier2": args.tier2}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        try:
+            ncpu = len(os.sched_getaffinity(0))
+        except Exception:
+            ncpu = os.cpu_count() or 1
+        workers = max(1, min(ncpu, 32, total_units))
+        rate, kind, detail = cpu_reference(args, total_units, K, W, workers)
+        line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+                "warmup": W, "ms_per_step": 1000.0 / rate, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": kind,
+                                 "sample": f"{workers} of {total_units} units (one per process, "
+                                           f"single-threaded) at {args.ctx} ctx, {args.q_per_kv} "
+                                           f"q-heads each, {K} timed steps after {W} warm-up; "
+                                           f"scaled x{total_units / workers:.1f}",
+                                 **detail},
+                "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        if os.environ.get("CKV_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2605_20868_b200 as ck
+    from paper_2605_20868_b200 import _lib
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    R = run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units,
+                e2e_wanted=not args.no_e2e)
+    ms, pa_ms, e2e, U = R["ms"], R["pa_ms"], R["e2e"], R["U"]
+    dec, cache, stats, last = R["dec"], R["cache"], R["stats"], R["last"]
+    pcie = pcie_stats(args, R, ms) if args.tier2 == "host" else None
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
     peak, peak_kind = peak_hbm()
-    tier1_bytes_launch = U * nb_timed * _lib.BLOCK_BYTES  # Tier-1 read by one pass A
+    tier1_bytes_launch = U * R["nb_timed"] * _lib.BLOCK_BYTES  # Tier-1 read by one pass A
     achieved = tier1_bytes_launch / (pa_ms / 1000.0) / 1e9
     step_bytes = total_units * args.ctx * 288.0
     step_frac = step_bytes / (ms / 1000.0) / 1e9 / peak
@@ -573,16 +678,24 @@ def main():
                      "peak_kind": peak_kind, "pass_a_ms": pa_ms},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": n_launch,
+        "gpu_launches": R["n_launch"],
         "k_star_mean": float(last["res"].cert["k_star"].mean()),
         "promoted_union_blocks_per_unit": float(dec.n_work.float().mean().item()),
-        "dense_heads_in_timed_region": n_dense,
+        "dense_heads_in_timed_region": R["n_dense"],
         "rung4_heads_in_timed_region": stats["rung4"],
         "value_promoted_per_head_mean": stats["nv"] / max(1, stats["steps"]),
         "pagein_bytes_per_step": stats["pagein"] / max(1, stats["steps"]),
-        "clocks": clocks,
-        "prefill_s": prefill_s,
+        "clocks": R["clocks"],
+        "prefill_s": R["prefill_s"],
     }
+    if pcie is not None:
+        line["pcie"] = pcie
+    if args.config == "c3" and world == 1 and not args.no_variant:
+        # the north-star placement of the same workload: Tier-2 in pinned host RAM,
+        # the reference's 2048-block scratch, misses over PCIe (bench --config c3host)
+        del R, dec, cache, last
+        torch.cuda.empty_cache()
+        line["variant_c3host"] = run_variant(args, ck, dev, dist, total_units)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
