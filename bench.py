@@ -74,6 +74,8 @@ def parse():
     ap.add_argument("--v-tol", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="shards plan their launches for the whole job (bit-identical to N=1)")
     ap.add_argument("--no-variant", action="store_true",
                     help="skip the c3host variant measured after the default c3 line")
     args = ap.parse_args()
@@ -295,8 +297,9 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
     my_units = sharding.shard_units(args.layers, args.kv_heads, args.batch, world, rank)
     # step-wide Rung 4 per (layer, sequence), shared by the ranks holding that layer's KV heads
     groups = np.asarray(list(my_units)) % (args.layers * args.batch)
+    det = dict(plan_units=total_units, dense_splits=64) if args.deterministic else {}
     dec = ck.CertifiedDecoder(cache, pol, n_heads=args.q_per_kv, scratch=scratch,
-                              rung4_group=groups)
+                              rung4_group=groups, **det)
     assert dec.n_groups == args.layers * args.batch
     nq = W + K
     qpool = torch.randn((nq, U, args.q_per_kv, 128), generator=g, device=dev, dtype=torch.float64)
@@ -311,7 +314,7 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
     reduce_flags = None
     if world > 1:
         def reduce_flags(flags):  # per-layer Rung-4 request, MAX over ranks (NCCL, no host sync)
-            dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+            sharding.reduce_group_flags(flags)
 
     def exchange():
         if world > 1:  # the bound report: outputs + certificates of every rank, one all-gather

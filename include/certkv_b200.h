@@ -180,6 +180,12 @@ typedef struct {
   int32_t epoch;            /* this step's epoch, < 2^27 (the caller increments it every step) */
   float stash_margin;       /* a block is stashed when some head's l'_b exceeds that head's
                                largest tail l' of the previous step minus this margin */
+  int32_t plan_units;       /* 0: launch-shape heuristics follow the units of the launch;
+                               > 0: they follow this many units (pass ckv_plan's n_units of
+                               the whole job so a shard computes bit for bit what the
+                               unsharded step computes for its units) */
+  int32_t dense_splits;     /* 0: dense splits per unit adapt to the number of dense units;
+                               > 0: fixed (independent of which other units are dense) */
 } ckv_step;
 
 #define CKV_SPLIT_FLOATS 136
@@ -210,6 +216,9 @@ typedef struct {
 
 /* Library / device info. */
 int32_t ckv_version(void);
+/* sizeof of the ABI structs as this library was compiled: out[0..4] = ckv_cache,
+ * ckv_policy, ckv_cert, ckv_step, ckv_scratch (lets a binding check its mirrors) */
+void ckv_struct_sizes(int32_t* out);
 int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity);
 /* Initialise both LRU states and zero the cumulative counters. */
 ckv_status ckv_scratch_init(int32_t n_units, int32_t max_blocks, const ckv_scratch* s, void* stream);

@@ -65,7 +65,7 @@ class CkvStep(ctypes.Structure):
                 ("ecap", I32), ("explore_n", P), ("explore_pos", P), ("unit_group", P),
                 ("group_flags", P), ("n_groups", I32), ("unit_done", P),
                 ("queue", P), ("stash", P), ("stash_epoch", P), ("epoch", I32),
-                ("stash_margin", ctypes.c_float)]
+                ("stash_margin", ctypes.c_float), ("plan_units", I32), ("dense_splits", I32)]
 
 
 class CkvScratch(ctypes.Structure):
@@ -91,6 +91,7 @@ def load():
     lib = ctypes.CDLL(LIB_PATH)
     sig = {
         "ckv_version": (I32, []),
+        "ckv_struct_sizes": (None, [P]),
         "ckv_lru_words": (I32, [I32, I32]),
         "ckv_scratch_init": (I32, [I32, I32, ctypes.POINTER(CkvScratch), P]),
         "ckv_plan": (I32, [I32, I32, I32, ctypes.POINTER(CkvPolicy), ctypes.POINTER(CkvStep)]),
@@ -129,7 +130,7 @@ def exported_symbols():
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
             "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
             "ckv_f64_to_f16", "ckv_last_error", "ckv_decode_begin", "ckv_decode_end",
-            "ckv_decode_flags", "ckv_decode_finish"]
+            "ckv_decode_flags", "ckv_decode_finish", "ckv_struct_sizes"]
 
 
 def check(code, what):

@@ -94,6 +94,15 @@ extern "C" {
 
 int32_t ckv_version(void) { return 100; }
 
+void ckv_struct_sizes(int32_t* out) {
+  if (!out) return;
+  out[0] = (int32_t)sizeof(ckv_cache);
+  out[1] = (int32_t)sizeof(ckv_policy);
+  out[2] = (int32_t)sizeof(ckv_cert);
+  out[3] = (int32_t)sizeof(ckv_step);
+  out[4] = (int32_t)sizeof(ckv_scratch);
+}
+
 int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity) {
   return ckv::lru_words(max_blocks, capacity);
 }

@@ -981,7 +981,8 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
   // few (unit, head) CTAs (e.g. 8-way KV-head sharding): 1024 threads per head, so
   // each CTA's serial phases are shorter; otherwise 256 threads, 4 CTAs per SM
-  const bool wide = (long long)nu * st->n_heads <= 2 * 148 && nbh <= 1024 * 8;
+  const long long plan_u = st->plan_units > 0 ? st->plan_units : nu;
+  const bool wide = plan_u * st->n_heads <= 2 * 148 && nbh <= 1024 * 8;
   if (wide)
     k_select<8, 1024><<<dim3(st->n_heads, nu), 1024, smS, s>>>(a);
   else if (nbh <= SEL_THREADS * 8)

@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   if (count == 0) return;
   // ~384 tasks in all: long splits (little merge work) when many units are dense,
   // up to DN_SPLITS per unit when only a few are (latency-bound otherwise)
-  a.n_dsplit = min(st.n_dsplit_cap, min(DN_SPLITS, max(32, (384 + count - 1) / count)));
+  a.n_dsplit = (st.dense_splits > 0) ? min(st.n_dsplit_cap, st.dense_splits)
+                                       : min(st.n_dsplit_cap, min(DN_SPLITS, max(32, (384 + count - 1) / count)));
   for (int task = blockIdx.x; task < count * a.n_dsplit; task += gridDim.x) {
   const int item = task / a.n_dsplit, sp = task % a.n_dsplit;
   const int e = st.dense_list[1 + c.n_units + item];

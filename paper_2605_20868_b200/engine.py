@@ -89,18 +89,26 @@ class CertifiedDecoder:
     ``rung4_group`` is the number of consecutive units that share a step-wide
     Rung 4 (a canary trip in any of them makes all their heads dense); the
     reference's single-layer run makes it every unit (harness.py:362-372).
+
+    ``plan_units`` / ``dense_splits``: by default the launch shapes adapt to this
+    decoder's unit count and to how many units turn dense in a step.  A shard of
+    a KV-head-sharded job that passes the whole job's unit count and a fixed
+    dense split count computes, for its units, bit for bit what one decoder over
+    every unit computes (the decomposition of every reduction is the same).
     """
 
     def __init__(self, cache: DeviceKVCache, policy: PolicyConfig, n_heads=4, scratch=None,
-                 rung4_group=None):
+                 rung4_group=None, plan_units=None, dense_splits=0):
         if not 1 <= n_heads <= _lib.MAX_QHEADS:
             raise ValueError("device path supports 1..4 query heads per KV head")
         self.cache, self.policy, self.nh = cache, policy, int(n_heads)
         self.lib = cache.lib
         self.pol_c = policy.to_c()
         st = _lib.CkvStep()
-        _lib.check(self.lib.ckv_plan(cache.n_units, cache.max_blocks, self.nh,
+        _lib.check(self.lib.ckv_plan(int(plan_units or cache.n_units), cache.max_blocks, self.nh,
                                      ctypes.byref(self.pol_c), ctypes.byref(st)), "ckv_plan")
+        st.plan_units = int(plan_units or 0)
+        st.dense_splits = int(dense_splits)
         U, NB, nh, dev = cache.n_units, cache.max_blocks, self.nh, cache.device
         self.q = torch.zeros((U, nh, D), dtype=torch.float64, device=dev)
         self.out = torch.zeros((U, nh, D), dtype=torch.float32, device=dev)

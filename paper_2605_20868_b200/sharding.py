@@ -53,13 +53,31 @@ def unpack_gathered(buf, world, n_local, n_heads, head_dim=128):
     return out, cert
 
 
+def _host_staged(t, group):
+    """gloo collectives run on host tensors: stage device tensors through RAM."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def gather_bound_report(out, cert_bytes, group=None):
-    """All-gather of the packed step (NCCL on GPU, gloo on CPU)."""
+    """All-gather of the packed step (NCCL over NVLink; gloo via host memory)."""
     world = dist.get_world_size(group)
     local = pack_step(out, cert_bytes)
-    buf = torch.empty(world * local.numel(), dtype=torch.uint8, device=local.device)
-    dist.all_gather_into_tensor(buf, local, group=group)
-    return buf
+    staged = _host_staged(local, group)
+    src = local.cpu() if staged else local
+    buf = torch.empty(world * src.numel(), dtype=torch.uint8, device=src.device)
+    dist.all_gather_into_tensor(buf, src, group=group)
+    return buf.to(local.device) if staged else buf
+
+
+def reduce_group_flags(flags, group=None):
+    """Step-wide Rung-4 requests, MAX over the ranks, in place (stream-ordered
+    with NCCL; host-staged with gloo)."""
+    if _host_staged(flags, group):
+        f = flags.cpu()
+        dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+        flags.copy_(f)
+    else:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
 
 
 def rung4_layers(flags_per_unit, layers_of_units, layers, group=None, device="cpu"):
