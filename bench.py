@@ -72,6 +72,9 @@ def parse():
     ap.add_argument("--scratch", type=int, default=None,
                     help="LRU scratch capacity in blocks (-1: every block, 0: off)")
     ap.add_argument("--v-tol", type=float, default=None)
+    ap.add_argument("--explore", type=float, default=0.0,
+                    help="exploration_rate of the policy (0 or 0.01..0.05; the reference default "
+                         "is 0.02, the paper's benchmarks run with 0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--deterministic", action="store_true",
@@ -237,7 +240,8 @@ def cpu_reference(args, total_units, steps, warmup, workers):
     from oracle import ref_arm
     if ref_arm.available():
         r = ref_arm.time_reference(args.ctx, args.q_per_kv, total_units, steps, warmup, workers,
-                                   v_tol=args.v_tol, adversarial=args.adversarial)
+                                   v_tol=args.v_tol, adversarial=args.adversarial,
+                                   explore=args.explore)
         return 1.0 / r["sec_per_step"], "reference", {
             "impl": "unmodified certkv (oracle/_ref) harness.run_workload, kernel backend "
                     f"'{r['backend']}'", "unit_step_s": r["round_s"], "prefill_s": r["prefill_s"],
@@ -289,8 +293,10 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
             cache.corrupt_offset(0, int(b), int(rs.integers(0, 128)),
                                  float(rs.choice([-1.0, 1.0]) * 5.0e4))
 
-    pol = ck.PolicyConfig(exploration_rate=0.0) if args.v_tol is None else \
-        ck.PolicyConfig(exploration_rate=0.0, v_tol=args.v_tol)
+    pkw = {"exploration_rate": args.explore}
+    if args.v_tol is not None:
+        pkw["v_tol"] = args.v_tol
+    pol = ck.PolicyConfig(**pkw)
     cap = cache.max_blocks if args.scratch < 0 else args.scratch
     scratch = ck.ScratchCache(cap) if args.scratch != 0 else None
     from paper_2605_20868_b200 import sharding
@@ -301,6 +307,8 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
     dec = ck.CertifiedDecoder(cache, pol, n_heads=args.q_per_kv, scratch=scratch,
                               rung4_group=groups, **det)
     assert dec.n_groups == args.layers * args.batch
+    if args.explore > 0:  # the spot check's generator, drawn from on the device every step
+        dec.attach_rng(np.random.Generator(np.random.Philox(np.random.SeedSequence((rank, 1)))))
     nq = W + K
     qpool = torch.randn((nq, U, args.q_per_kv, 128), generator=g, device=dev, dtype=torch.float64)
     kpool = torch.randn((nq, U, 1, 128), generator=g, device=dev).half()
@@ -548,17 +556,18 @@ def pcie_stats(args, R, ms):
                     "slots) and by k_dense (dense rungs); peak = pinned DMA H2D of 256 MB"}
 
 
-def run_variant(args, ck, dev, dist, total_units, name="c3host", K=8, W=3):
+def run_variant(args, ck, dev, dist, total_units, name="c3host", K=8, W=3, explore=0.0):
     """Another preset on the same box after the main line (fewer steps)."""
     import copy
     va = copy.copy(args)
     pre = PRESETS[name]
     for k in ("ctx", "batch", "tier2", "scratch", "v_tol"):
         setattr(va, k, pre[k])
-    va.adversarial, va.desc, va.config = pre["adversarial"], pre["desc"], name
+    va.adversarial, va.desc, va.config, va.explore = pre["adversarial"], pre["desc"], name, explore
     R = run_gpu(va, ck, dev, 1, 0, 0, K, W, dist, total_units, e2e_wanted=False,
                 clocks_wanted=False)
-    out = {"workload": pre["desc"], "value": 1000.0 / R["ms"], "unit": UNIT,
+    out = {"workload": pre["desc"] + (f", exploration_rate {explore} (device draws)" if explore else ""),
+           "value": 1000.0 / R["ms"], "unit": UNIT,
            "ms_per_step": R["ms"], "steps": K, "warmup": W, "pass_a_ms": R["pa_ms"],
            "hbm_frac_step": total_units * va.ctx * 288.0 / (R["ms"] / 1000.0) / 1e9 / peak_hbm()[0],
            "dense_heads_in_timed_region": R["n_dense"]}
@@ -580,9 +589,9 @@ def main():
         local = 0
     K, W = args.steps, max(3, args.warmup)
     total_units = args.layers * args.kv_heads * args.batch
-    pol_desc = "PolicyConfig(exploration_rate=0.0) defaults"
+    pol_desc = f"PolicyConfig(exploration_rate={args.explore}) defaults"
     if args.v_tol is not None:
-        pol_desc = f"PolicyConfig(exploration_rate=0.0, v_tol={args.v_tol})"
+        pol_desc = f"PolicyConfig(exploration_rate={args.explore}, v_tol={args.v_tol})"
     tier1_gb = total_units * args.ctx * 288 / 1e9
     config = {"workload": args.desc if args.ctx == PRESETS[args.config]["ctx"] else
               f"{args.config.upper()} shape at {args.ctx} ctx, batch {args.batch}",
@@ -699,6 +708,9 @@ def main():
         del R, dec, cache, last
         torch.cuda.empty_cache()
         line["variant_c3host"] = run_variant(args, ck, dev, dist, total_units)
+        torch.cuda.empty_cache()
+        line["variant_c3_explore"] = run_variant(args, ck, dev, dist, total_units, name="c3",
+                                                 explore=0.02)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

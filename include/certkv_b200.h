@@ -186,7 +186,16 @@ typedef struct {
                                unsharded step computes for its units) */
   int32_t dense_splits;     /* 0: dense splits per unit adapt to the number of dense units;
                                > 0: fixed (independent of which other units are dense) */
+  uint64_t* explore_rng;    /* [16] numpy Philox4x64 generator state (counter[4], key[2],
+                               buffer[4], buffer_pos, has_uint32, uinteger): when set, the
+                               exploration samples are drawn on the device from it, in the
+                               reference's stream order, and it is advanced in place;
+                               NULL: explore_n / explore_pos hold host-drawn samples */
+  double explore_rate;      /* exploration_rate of the policy (device draws) */
+  int32_t* explore_work;    /* [CKV_EXPLORE_WORK(n_units * n_heads)] device-draw scratch */
 } ckv_step;
+
+#define CKV_EXPLORE_WORK(items) (4 * (items) + 64)
 
 #define CKV_SPLIT_FLOATS 136
 #define CKV_HEAD_FLOATS 288

@@ -46,7 +46,7 @@ def _import_certkv():
     return certkv
 
 
-def _init(ctx, q_per_kv, seed, n_steps, v_tol, adversarial):
+def _init(ctx, q_per_kv, seed, n_steps, v_tol, adversarial, explore=0.0):
     _limit_threads()
     import numpy as np
     certkv = _import_certkv()
@@ -68,8 +68,8 @@ def _init(ctx, q_per_kv, seed, n_steps, v_tol, adversarial):
                          kv_heads=1, steps=n_steps, seed=seed, ingest_binary16=True)
     wl = Workload(cfg, [cache], queries, keys[ctx:, None, :].astype(np.float32),
                   values[ctx:, None, :].astype(np.float32))
-    pol = PolicyConfig(exploration_rate=0.0) if v_tol is None else \
-        PolicyConfig(exploration_rate=0.0, v_tol=v_tol)
+    pol = PolicyConfig(exploration_rate=explore) if v_tol is None else \
+        PolicyConfig(exploration_rate=explore, v_tol=v_tol)
     _W.update(wl=wl, pol=pol, next=0, prefill_s=time.perf_counter() - t0,
               backend=certkv._kernels.get_backend().NAME)
 
@@ -111,8 +111,8 @@ def host_info():
 
 
 def _worker(w, args, barrier, out):
-    ctx, q_per_kv, seed, n, v_tol, adversarial, warmup, steps = args
-    _init(ctx, q_per_kv, seed + w, n, v_tol, adversarial)
+    ctx, q_per_kv, seed, n, v_tol, adversarial, warmup, steps, explore = args
+    _init(ctx, q_per_kv, seed + w, n, v_tol, adversarial, explore)
     barrier.wait()
     if warmup:
         _run(warmup)
@@ -121,7 +121,7 @@ def _worker(w, args, barrier, out):
 
 
 def time_reference(ctx, q_per_kv, total_units, steps, warmup, workers, v_tol=None,
-                   adversarial=False, seed=1234):
+                   adversarial=False, seed=1234, explore=0.0):
     """Seconds per full decode step (``total_units`` unit-steps) of the unmodified
     reference: ``workers`` processes (one unit each) run ``warmup`` then ``steps``
     steps concurrently; the slowest worker's time counts."""
@@ -129,7 +129,7 @@ def time_reference(ctx, q_per_kv, total_units, steps, warmup, workers, v_tol=Non
     ctxm = mp.get_context("fork")
     barrier = ctxm.Barrier(workers)
     out = ctxm.Queue()
-    args = (ctx, q_per_kv, seed, warmup + steps, v_tol, adversarial, warmup, steps)
+    args = (ctx, q_per_kv, seed, warmup + steps, v_tol, adversarial, warmup, steps, explore)
     procs = [ctxm.Process(target=_worker, args=(w, args, barrier, out)) for w in range(workers)]
     for p in procs:
         p.start()

@@ -68,6 +68,7 @@ cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, 
 cudaError_t launch_dense(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, cudaStream_t);
 cudaError_t launch_group_flags(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
+cudaError_t launch_explore_draw(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
 cudaError_t launch_lru_init(int32_t*, int, int, int, cudaStream_t);
 cudaError_t launch_block_logmass(const double*, const int64_t*, int, double*, double*, double*,
@@ -192,6 +193,13 @@ ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step*
                             int32_t host_max_blocks, void* stream) {
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   cudaError_t e = cudaSuccess;
+  if (st->explore_rng) {  // exploration samples drawn on the device (explore_draw.cu)
+    if (!st->explore_n || !st->explore_pos || !st->explore_work || st->ecap <= 0 ||
+        !(st->explore_rate > 0.0))
+      return CKV_EINVAL;
+    e = ckv::launch_explore_draw(c, st, S(stream));
+    if (e != cudaSuccess) return st_of(e);
+  }
   if (st->explore_n) {
     if (!st->explore_pos || st->ecap <= 0) return CKV_EINVAL;
     e = ckv::launch_explore(c, pol, st, host_max_blocks, S(stream));
@@ -220,7 +228,9 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
   ckv_status r = ckv_decode_begin(c, pol, st, scratch, host_max_blocks, stream);
   if (r != CKV_OK) return r;
   int32_t* en = st->explore_n;
-  st->explore_n = nullptr;  // samples need the begin half's K': use begin/end for exploration
+  // host-drawn samples need the begin half's K' first (begin / end); device draws
+  // (explore_rng) happen in stream order inside the step
+  if (!st->explore_rng) st->explore_n = nullptr;
   r = ckv_decode_end(c, pol, st, scratch, host_max_blocks, stream);
   st->explore_n = en;
   return r;

@@ -58,8 +58,8 @@ class StepOutput:
 class PendingStep:
     """Handle of a step enqueued by ``CertifiedDecoder.step_async``."""
 
-    def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens):
-        self._args = (cert_h, stat_h, ps_h, n_tokens)
+    def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens, en_h=None):
+        self._args = (cert_h, stat_h, ps_h, n_tokens, en_h)
         self._dec, self._ev, self._res, self._exc = dec, event, None, None
 
     def done(self):
@@ -133,7 +133,12 @@ class CertifiedDecoder:
         self.explore_n = torch.zeros((U, nh), dtype=torch.int32, device=dev)
         self.explore_pos = torch.zeros((U, nh, st.ecap), dtype=torch.int32, device=dev)
         self.explore_n_host = torch.zeros((U, nh), dtype=torch.int32).pin_memory()
-        self.explore_pos_host = torch.zeros((U, nh, st.ecap), dtype=torch.int32).pin_memory()
+        self.rng_words = torch.zeros((16,), dtype=torch.int64, device=dev)
+        self.rng_host = torch.zeros((16,), dtype=torch.int64).pin_memory()
+        self.explore_work = torch.zeros((4 * U * nh + 64,), dtype=torch.int32, device=dev)
+        self._attached = None
+        st.explore_rate = float(policy.exploration_rate)
+        st.explore_work = _ptr(self.explore_work)
         self.dense_part = torch.zeros((U, st.n_dsplit_cap, 4, 132), dtype=torch.float32, device=dev)
         for name, t in (("q", self.q), ("out", self.out), ("cert", self.cert_buf),
                         ("lm1", self.lm1), ("split_state", self.split_state),
@@ -184,7 +189,7 @@ class CertifiedDecoder:
         self.ps_host = torch.zeros((U, 4), dtype=torch.int32).pin_memory()
 
     # -- the device step -----------------------------------------------------
-    def launch(self, queries=None, reduce_flags=None):
+    def launch(self, queries=None, reduce_flags=None, explore=False):
         """Enqueue the whole step (no host sync); returns immediately.
 
         ``reduce_flags(group_flags)`` -- e.g. an all-reduce(MAX) across the
@@ -196,6 +201,9 @@ class CertifiedDecoder:
         args = (ctypes.byref(self.cache.c), ctypes.byref(self.pol_c), ctypes.byref(self.st))
         nbk, stream = self.cache.num_blocks, _stream(self.cache.device)
         self.st.epoch = (self.st.epoch + 1) & 0x3ffffff
+        # exploration: samples drawn on the device from the generator state in rng_words
+        self.st.explore_rng = _ptr(self.rng_words) if explore else None
+        self.st.explore_n = _ptr(self.explore_n) if explore else None
         if reduce_flags is None:
             _lib.check(self.lib.ckv_decode_step(*args, sc, nbk, stream), "ckv_decode_step")
             return
@@ -211,18 +219,51 @@ class CertifiedDecoder:
         The fast path, the step-wide Rung 4 resolution and the dense fallback
         all run on the device; the host reads back the certificate array once
         (and raises on a Tier-2 loss).  With ``policy.exploration_rate > 0``
-        and a NumPy Generator ``rng`` the exploration spot check runs between
-        the two halves of the step: the host draws the sampled tail positions
-        from ``rng`` exactly as fallback.py:212-218 does (heads in unit-major
-        q-head order) and the device rescores those blocks.
+        and the workload's numpy Philox Generator ``rng`` the exploration spot
+        check runs too: the device draws the sampled tail positions from the
+        generator's state exactly as fallback.py:212-218 does (heads in
+        unit-major q-head order; csrc/explore_draw.cu), rescores those blocks,
+        and ``rng`` is advanced as the reference's draws would advance it.
         """
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
-        self.explore_counts = None
-        if self.policy.exploration_rate > 0 and rng is not None:
-            return self._step_explore(queries, rng)
-        self.launch(queries)
-        return self._finish()
+        explore = self.policy.exploration_rate > 0 and rng is not None
+        if explore and self._attached is None:
+            self._rng_upload(rng)
+        self.launch(queries, explore=explore or self._attached is not None)
+        out = self._finish(explore or self._attached is not None)
+        if explore and self._attached is None:
+            self._rng_download(rng)
+        return out
+
+    # -- exploration generator on the device ------------------------------------
+    def _rng_upload(self, rng):
+        if not isinstance(getattr(rng, "bit_generator", None), np.random.Philox):
+            raise ValueError("the exploration generator must be a numpy Generator over Philox "
+                             "(the reference's philox4x64 stream, harness.py:93-95)")
+        self.rng_host.numpy()[:] = pack_philox_state(rng.bit_generator.state).view(np.int64)
+        self.rng_words.copy_(self.rng_host, non_blocking=True)
+
+    def _rng_download(self, rng):
+        self.rng_host.copy_(self.rng_words)  # synchronous
+        st = rng.bit_generator.state
+        rng.bit_generator.state = unpack_philox_state(self.rng_host.numpy().view(np.uint64), st)
+
+    def attach_rng(self, rng):
+        """Keep the exploration generator on the device across steps (step_async
+        with exploration): the state is uploaded once and advanced by every
+        step; ``detach_rng`` writes it back into ``rng``."""
+        if self.policy.exploration_rate <= 0:
+            raise ValueError("the policy's exploration_rate is 0")
+        self._rng_upload(rng)
+        self._attached = rng
+
+    def detach_rng(self):
+        rng, self._attached = self._attached, None
+        if rng is not None:
+            torch.cuda.current_stream(self.cache.device).synchronize()
+            self._rng_download(rng)
+        return rng
 
     def step_async(self, queries, reduce_flags=None):
         """Enqueue a certified step and return a ``PendingStep`` without a host
@@ -230,42 +271,49 @@ class CertifiedDecoder:
         behind the step's kernels, so the host can read step i's bound report
         while the device runs step i+1.  The output stays on the device
         (``self.out``, valid in stream order until the next step overwrites
-        it); dense rungs are already applied there."""
+        it); dense rungs are already applied there.  Exploration runs when a
+        generator is attached (``attach_rng``)."""
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
-        if self.policy.exploration_rate > 0:
-            raise ValueError("step_async does not run the exploration spot check; use step()")
-        self.launch(queries, reduce_flags)
+        explore = self._attached is not None
+        self.launch(queries, reduce_flags, explore=explore)
         k = self._ring_i = (getattr(self, "_ring_i", 1) + 1) % 2
         if not hasattr(self, "_ring"):
             shp = self.cert_host.shape
             self._ring = [(torch.zeros(shp, dtype=torch.uint8).pin_memory(),
                            torch.zeros((8,), dtype=torch.int32).pin_memory(),
                            torch.zeros(self.ps_host.shape, dtype=torch.int32).pin_memory(),
+                           torch.zeros(self.explore_n.shape, dtype=torch.int32).pin_memory(),
                            torch.cuda.Event()) for _ in range(2)]
             self._ring_pending = [None, None]
         prev = self._ring_pending[k]
         if prev is not None:
             prev._decode()  # decode the step that last used this buffer before reusing it
-        cert_h, stat_h, ps_h, ev = self._ring[k]
+        cert_h, stat_h, ps_h, en_h, ev = self._ring[k]
         cert_h.copy_(self.cert_buf, non_blocking=True)
         stat_h.copy_(self.cache.status, non_blocking=True)
         if self.scratch is not None:
             ps_h.copy_(self.page_stats, non_blocking=True)
+        if explore:
+            en_h.copy_(self.explore_n, non_blocking=True)
         ev.record(torch.cuda.current_stream(self.cache.device))
-        pend = PendingStep(self, cert_h, stat_h, ps_h, ev, self.cache.num_tokens)
+        pend = PendingStep(self, cert_h, stat_h, ps_h, ev, self.cache.num_tokens,
+                           en_h if explore else None)
         self._ring_pending[k] = pend
         return pend
 
-    def _finish(self):
+    def _finish(self, explore=False):
         self.cert_host.copy_(self.cert_buf, non_blocking=True)
         self.status_host.copy_(self.cache.status, non_blocking=True)
         if self.scratch is not None:
             self.ps_host.copy_(self.page_stats, non_blocking=True)
+        if explore:
+            self.explore_n_host.copy_(self.explore_n, non_blocking=True)
         torch.cuda.current_stream(self.cache.device).synchronize()  # the step's only host sync
-        return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens)
+        return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens,
+                            self.explore_n_host if explore else None)
 
-    def _output(self, cert_h, stat_h, ps_h, n_tokens):
+    def _output(self, cert_h, stat_h, ps_h, n_tokens, en_h=None):
         if self.cache.take_rejections(stat_h):  # a deferred append check (DeviceKVCache.append)
             self.cache.resync()
             raise ValueError("non-finite key/value entry (append rejected on the device)")
@@ -278,47 +326,35 @@ class CertifiedDecoder:
         n_units = int(np.isin(self.unit_group_host, flagged).sum()) if flagged.size else 0
         staging = n_units * 2 * n_tokens * D * 2
         ps = ps_h.numpy().copy() if self.scratch is not None else None
-        return StepOutput(self.out, cert, kinds, ps, staging, self)
-
-    def _step_explore(self, queries, rng):
-        if queries is not None:
-            self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
-        stream = _stream(self.cache.device)
-        nbk = self.cache.num_blocks
-        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
-        self.st.epoch = (self.st.epoch + 1) & 0x3ffffff
-        _lib.check(self.lib.ckv_decode_begin(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                             ctypes.byref(self.st), sc, nbk, stream), "ckv_decode_begin")
-        self.cert_host.copy_(self.cert_buf, non_blocking=True)
-        torch.cuda.current_stream(self.cache.device).synchronize()
-        cert = self.cert_host.numpy().view(CERT_DTYPE).reshape(self.cache.n_units, self.nh)
-        en = self.explore_n_host.numpy()
-        ep = self.explore_pos_host.numpy()
-        en[:] = 0
-        rate = self.policy.exploration_rate
-        for u in range(self.cache.n_units):
-            for j in range(self.nh):
-                if not nbk:
-                    continue
-                n_tail = nbk - int(cert[u, j]["k_star"])
-                count = min(n_tail, int(round(rate * nbk)))
-                if count == 0:
-                    continue
-                chosen = np.sort(rng.choice(n_tail, size=count, replace=False))
-                en[u, j] = count
-                ep[u, j, :count] = chosen
-        self.explore_n.copy_(self.explore_n_host, non_blocking=True)
-        self.explore_pos.copy_(self.explore_pos_host, non_blocking=True)
-        self.st.explore_n = _ptr(self.explore_n)
-        sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
-        code = self.lib.ckv_decode_end(ctypes.byref(self.cache.c), ctypes.byref(self.pol_c),
-                                       ctypes.byref(self.st), sc, nbk, stream)
-        self.st.explore_n = None
-        _lib.check(code, "ckv_decode_end")
-        out = self._finish()
-        self.explore_counts = en.copy()
-        out.explore_counts = self.explore_counts
+        out = StepOutput(self.out, cert, kinds, ps, staging, self)
+        if en_h is not None:
+            out.explore_counts = en_h.numpy().copy()
         return out
+
+
+def pack_philox_state(state):
+    """numpy Philox bit_generator.state -> the 16 uint64 words of
+    ckv_step.explore_rng (counter, key, buffer, buffer_pos, has_uint32, uinteger)."""
+    w = np.zeros(16, dtype=np.uint64)
+    w[0:4] = np.asarray(state["state"]["counter"], dtype=np.uint64)
+    w[4:6] = np.asarray(state["state"]["key"], dtype=np.uint64)
+    w[6:10] = np.asarray(state["buffer"], dtype=np.uint64)
+    w[10] = int(state["buffer_pos"])
+    w[11] = int(state["has_uint32"])
+    w[12] = int(state["uinteger"])
+    return w
+
+
+def unpack_philox_state(words, template):
+    """Inverse of pack_philox_state, into a copy of ``template``."""
+    st = dict(template)
+    st["state"] = {"counter": np.asarray(words[0:4], dtype=np.uint64).copy(),
+                   "key": np.asarray(words[4:6], dtype=np.uint64).copy()}
+    st["buffer"] = np.asarray(words[6:10], dtype=np.uint64).copy()
+    st["buffer_pos"] = int(words[10])
+    st["has_uint32"] = int(words[11])
+    st["uinteger"] = int(words[12])
+    return st
 
 
 # -- reference-shaped per-head API --------------------------------------------
