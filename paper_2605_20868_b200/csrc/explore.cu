@@ -11,8 +11,27 @@
 
 namespace ckv {
 
-__global__ void __launch_bounds__(128) k_explore(StepArgs a) {
-  extern __shared__ __align__(16) uint32_t sh[];
+constexpr int XP_WARPS = 4;
+constexpr int XP_STAGES = 3;
+constexpr int XP_KEY = OFF_VCODES;  // key codes + scale + offset: the head of the record
+constexpr int XP_STAGE = XP_KEY + B * D * 2;  // + the FP16 original key tile
+
+struct ExploreSmem {
+  uint8_t stage[XP_WARPS][XP_STAGES][XP_STAGE];
+  uint64_t bar[XP_WARPS][XP_STAGES];
+  float qh[H * D];
+};
+
+// One CTA per (unit, q-head).  The sampled tail positions are mapped to block
+// ids first (promoted bitmap + per-word tail prefix), then every warp streams
+// its blocks through a 3-stage ring of bulk copies -- the key part of the
+// Tier-1 record (3 KB) and the FP16 original key tile (4 KB) per block -- and
+// compares the Phase-1 scores (phase1_block) with the original-key scores
+// (orig_block): a gap above Delta + epsilon_guard is a canary event.
+__global__ void __launch_bounds__(XP_WARPS * 32) k_explore(StepArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  ExploreSmem& S = *reinterpret_cast<ExploreSmem*>(smem_raw);
+  uint32_t* fb = reinterpret_cast<uint32_t*>(smem_raw + sizeof(ExploreSmem));  // [W] promoted
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const ckv_policy& pol = a.pol;
@@ -24,40 +43,48 @@ __global__ void __launch_bounds__(128) k_explore(StepArgs a) {
   if (n <= 0) return;
   const int nb = c.n_blocks[u];
   const int W = (nb + 31) / 32;
-  uint32_t* fb = sh;               // [W] promoted bitmap
-  uint32_t* pre = sh + W;          // [W] tail blocks before word w
-  __shared__ __align__(16) float qh[H * D];
+  uint32_t* pre = fb + W;                                    // [W] tail blocks before word w
+  int32_t* blk = reinterpret_cast<int32_t*>(pre + W);        // [n] sampled block ids
   __shared__ int fail;
   for (int i = tid; i < W; i += blockDim.x) fb[i] = 0u;
   for (int i = tid; i < H * D; i += blockDim.x) {
     const int hh = i / D;
-    qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845) : 0.f;
+    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845) : 0.f;
   }
-  if (tid == 0) fail = 0;
+  if (tid == 0) {
+    fail = 0;
+    for (int w = 0; w < XP_WARPS; ++w)
+      for (int s = 0; s < XP_STAGES; ++s) mbar_init(&S.bar[w][s], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
   const int kp = st.cert[hu].k_star;
   const int32_t* ord = st.order + hu * st.kcap;
   for (int i = tid; i < kp; i += blockDim.x) atomicOr(&fb[ord[i] >> 5], 1u << (ord[i] & 31));
   __syncthreads();
-  if (tid == 0) {  // exclusive prefix of tail counts per 32-block word
-    int run = 0;
-    for (int w = 0; w < W; ++w) {
-      pre[w] = run;
-      const uint32_t valid = (w == W - 1 && (nb & 31)) ? ((1u << (nb & 31)) - 1u) : 0xffffffffu;
-      run += __popc(~fb[w] & valid);
+  if (warp == 0) {  // exclusive prefix of the tail counts per 32-block word
+    int carry = 0;
+    for (int w0 = 0; w0 < W; w0 += 32) {
+      const int w = w0 + lane;
+      int cnt = 0;
+      if (w < W) {
+        const uint32_t valid = (w == W - 1 && (nb & 31)) ? ((1u << (nb & 31)) - 1u) : 0xffffffffu;
+        cnt = __popc(~fb[w] & valid);
+      }
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (w < W) pre[w] = carry + x - cnt;
+      carry += __shfl_sync(0xffffffffu, x, 31);
     }
   }
   __syncthreads();
-  QFrag f;
-  load_qfrag(f, qh, lane);
-  QFrag16 f16;
-  load_qfrag16(f16, qh, lane);
-  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
-  const double thr = (double)hs.delta + pol.epsilon_guard;
-  const size_t ubk = (size_t)u * c.max_blocks;
+  // tail position -> block: binary search the word, then the bit
   const int32_t* pos = st.explore_pos + hu * st.ecap;
-  for (int i = warp; i < n; i += blockDim.x / 32) {
-    // block id of tail position pos[i]: binary search the word, then the bit
+  for (int i = tid; i < n; i += blockDim.x) {
     const int p = pos[i];
     int lo = 0, hi = W - 1;
     while (lo < hi) {
@@ -67,16 +94,43 @@ __global__ void __launch_bounds__(128) k_explore(StepArgs a) {
     uint32_t m = ~fb[lo];
     int r = p - (int)pre[lo];
     while (r-- > 0) m &= m - 1u;
-    const int b = lo * 32 + __ffs(m) - 1;
+    blk[i] = lo * 32 + __ffs(m) - 1;
+  }
+  __syncthreads();
+  const size_t ubk = (size_t)u * c.max_blocks;
+  const int nmine = (n > warp) ? (n - warp + XP_WARPS - 1) / XP_WARPS : 0;
+  auto issue = [&](int i, int s) {
+    const int b = blk[warp + XP_WARPS * i];
+    mbar_expect_tx(&S.bar[warp][s], XP_STAGE);
+    bulk_g2s(S.stage[warp][s], c.tier1 + (ubk + b) * REC, XP_KEY, &S.bar[warp][s]);
+    bulk_g2s(S.stage[warp][s] + XP_KEY, c.tier2_k + (ubk + b) * B * D, B * D * 2, &S.bar[warp][s]);
+  };
+  if (lane == 0)
+    for (int s = 0; s < XP_STAGES && s < nmine; ++s) issue(s, s);
+  QFrag f;
+  load_qfrag(f, S.qh, lane);
+  QFrag16 f16;
+  load_qfrag16(f16, S.qh, lane);
+  const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+  const double thr = (double)hs.delta + pol.epsilon_guard;
+  bool bad = false;
+  for (int i = 0; i < nmine; ++i) {
+    const int s = i % XP_STAGES;
+    const int b = blk[warp + XP_WARPS * i];
     if (lane == 0 && !c.tier2_valid[ubk + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
-    const BlockScores q = phase1_block(f, c.tier1 + (ubk + b) * REC, c.kscale_max[ubk + b], lane);
-    const float2 o = orig_block(f16, reinterpret_cast<const uint4*>(c.tier2_k + (ubk + b) * B * D), lane);
+    mbar_wait(&S.bar[warp][s], (uint32_t)(i / XP_STAGES) & 1u);
+    const uint8_t* st8 = S.stage[warp][s];
+    const BlockScores q = phase1_block(f, st8, c.kscale_max[ubk + b], lane);
+    const float2 o = orig_block(f16, reinterpret_cast<const uint4*>(st8 + XP_KEY), lane);
     float gap = fmaxf(fabsf(o.x - q.s0), fabsf(o.y - q.s1));
     gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 4));
     gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 8));
     gap = fmaxf(gap, __shfl_xor_sync(0xffffffffu, gap, 16));
-    if (lane == h && !((double)gap <= thr)) fail = 1;
+    bad |= (lane == h && !((double)gap <= thr));
+    __syncwarp();  // every lane is done with the stage before it is refilled
+    if (lane == 0 && i + XP_STAGES < nmine) issue(i + XP_STAGES, s);
   }
+  if (bad) fail = 1;
   __syncthreads();
   if (tid == 0 && fail) {
     ckv_cert& ct = st.cert[hu];
@@ -90,7 +144,10 @@ cudaError_t launch_explore(const ckv_cache* c, const ckv_policy* pol, const ckv_
                            int host_max_blocks, cudaStream_t s) {
   StepArgs a{*c, *st, *pol};
   const int W = (host_max_blocks + 31) / 32;
-  k_explore<<<dim3(st->n_heads, c->n_units), 128, 2 * W * 4, s>>>(a);
+  const size_t smem = sizeof(ExploreSmem) + (size_t)2 * W * 4 + (size_t)st->ecap * 4;
+  cudaError_t e = set_max_dyn_smem(k_explore, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_explore<<<dim3(st->n_heads, c->n_units), XP_WARPS * 32, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -256,8 +256,10 @@ __device__ int draw_head(const RngState& S, const Head& H, long long off, int2* 
       k_after = kk;
       nres = L + 1;
     }
-    // bookkeeping in call order (lane-serial; the map is shared by the warp)
-    for (int l = 0; l < nres; ++l) {
+    // bookkeeping in call order (lane-serial; the map is shared by the warp); the
+    // Floyd shuffle's draws only advance the stream
+    const int nbook = H.tail ? nres : max(0, min(nres, H.size - t0));
+    for (int l = 0; l < nbook; ++l) {
       const int tt = t0 + l;
       const uint32_t v = (l == L) ? vL : __shfl_sync(0xffffffffu, val, l);
       if (lane == 0) {
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(XD_MAX_WARPS * 32) k_explore_draw(DrawArgs a) 
   // work words: rej[items], off_lo/hi[items] (int64 as two words), flags[XD_ITERS + 2]
   int32_t* rej = st.explore_work;
   long long* off = reinterpret_cast<long long*>(st.explore_work + ((a.items + 1) & ~1));
-  int32_t* flags = reinterpret_cast<int32_t*>(off + a.items);
+  int32_t* flags = reinterpret_cast<int32_t*>(off + a.items + 1);
   const int n = a.items;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) rej[i] = 0;
   if (blockIdx.x == 0 && threadIdx.x < XD_ITERS + 2) flags[threadIdx.x] = 0;
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(XD_MAX_WARPS * 32) k_explore_draw(DrawArgs a) 
         off[i] = run;
         run += head_of(c, st, i).base + __ldcg(rej + i);
       }
+      if (threadIdx.x == blockDim.x - 1) off[n] = run;  // every draw of the step
     }
     grid.sync();
     for (int i = gw; i < n; i += nwarps) {
@@ -374,8 +377,11 @@ __global__ void __launch_bounds__(XD_MAX_WARPS * 32) k_explore_draw(DrawArgs a) 
     grid.sync();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {  // the generator's state after every draw
-    long long T = 0;
-    for (int i = 0; i < n; ++i) T += head_of(c, st, i).base + __ldcg(rej + i);
+    long long T = __ldcg(off + n);
+    if (!done) {  // the sequential pass fixed the rejections: recount
+      T = 0;
+      for (int i = 0; i < n; ++i) T += head_of(c, st, i).base + __ldcg(rej + i);
+    }
     uint64_t o[13];
     advance(S, (uint64_t)T, o);
     for (int i = 0; i < 13; ++i) st.explore_rng[i] = o[i];
