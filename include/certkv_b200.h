@@ -136,8 +136,9 @@ typedef struct {
 /* Caller-owned per-step buffers (device memory). */
 typedef struct {
   int32_t n_heads;          /* active q-heads per unit, 1..4 */
-  int32_t n_splits;         /* pass-A splits per unit (from ckv_plan) */
-  int32_t blocks_per_split;
+  int32_t n_splits;         /* pass-A split capacity per unit (from ckv_plan); each step
+                               partitions a unit's blocks over at most this many */
+  int32_t blocks_per_split; /* the smallest split ckv_plan sized the capacity for */
   int32_t kcap;             /* promoted-list capacity per head (>= 2*k_max+1) */
   int32_t wcap;             /* work-list capacity per head (kcap + max_blocks) */
   int32_t n_chunks;         /* pass-B chunks per head */

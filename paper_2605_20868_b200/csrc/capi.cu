@@ -12,6 +12,8 @@ const Knobs& knobs() {
     r.separate_pagein = getenv("CKV_SEPARATE_PAGEIN") != nullptr;
     const char* ch = getenv("CKV_CHUNKS");
     r.chunks = ch ? atoi(ch) : 1;
+    r.sel_kpt = r.sel_nt = 0;
+    if (const char* sv = getenv("CKV_SEL")) sscanf(sv, "%d:%d", &r.sel_kpt, &r.sel_nt);
     return r;
   }();
   return k;
@@ -129,12 +131,9 @@ ckv_status ckv_plan(int32_t n_units, int32_t max_blocks, int32_t n_heads, const 
   if (pol->k_max < 0 || pol->k_min < 0 || pol->k_max < pol->k_min || pol->k_max > 511 ||
       pol->ranking_depth < 1 || pol->ranking_depth > 64)
     return CKV_EINVAL;
-  long long work = (long long)n_units * max_blocks / 1184;
-#ifndef CKV_PA_BPS
-#define CKV_PA_BPS 256
-#endif
-  int bps = CKV_PA_BPS;
-  while (bps > 16 && bps > work) bps >>= 1;
+  /* pass-A split capacity: splits of >= 64 blocks; the launch picks how many it
+     uses (pa_splits in decode.cu) */
+  const int bps = 64;
   st->n_heads = n_heads;
   st->blocks_per_split = bps;
   st->n_splits = (max_blocks + bps - 1) / bps;

@@ -89,6 +89,7 @@ struct Knobs {
   bool separate_lru;     // CKV_SEPARATE_LRU: k_lru_fast instead of the LRU fused into pass B
   bool separate_pagein;  // CKV_SEPARATE_PAGEIN: gather kernel on a side stream before pass B
   int chunks;            // CKV_CHUNKS: unit-chunked overlap of the tail with pass A
+  int sel_kpt, sel_nt;   // CKV_SEL=kpt:nt forces a k_select variant (A/B runs)
 };
 const Knobs& knobs();
 struct DevState {

@@ -111,8 +111,11 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
   const int nb = c.n_blocks[u];
-  const int b0 = sp * st.blocks_per_split;
-  const int b1 = min(nb, b0 + st.blocks_per_split);
+  // balanced partition of the unit's blocks over its splits (pa_splits)
+  const int nsp = min(a.nsplit, nb);
+  if (sp >= nsp) return;
+  const int b0 = (int)((long long)sp * nb / nsp);
+  const int b1 = (int)((long long)(sp + 1) * nb / nsp);
 
   for (int i = tid; i < H * D; i += blockDim.x) {
     int h = i / D;
@@ -400,7 +403,7 @@ template <int KPT, int NT>
 #ifndef SEL_MINB
 #define SEL_MINB 4  // 64 registers (some spills) but 32 warps per SM: measured faster than 2
 #endif
-__global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArgs a) {
+__global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)) k_select(StepArgs a) {
 #ifdef CKV_SELPROF
   unsigned long long t_prev = gtimer();
 #endif
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
   if (tid == 0) {
     prefetch_l2(c.eta + (size_t)u * c.max_blocks, (uint32_t)nb * 4u);
     prefetch_l2(st.split_state + (size_t)u * st.n_splits * H * CKV_SPLIT_FLOATS,
-                (uint32_t)((nb + st.blocks_per_split - 1) / st.blocks_per_split) * H * CKV_SPLIT_FLOATS * 4u);
+                (uint32_t)min(a.nsplit, nb) * H * CKV_SPLIT_FLOATS * 4u);
   }
   // ---- this thread's blocks tid + NT * j (j < KPT): order keys of l'_b in
   // registers; strided ownership keeps every load coalesced
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : 1) k_select(StepArg
 
   SELPROF(2);
   // ---- merge the pass-A splits: headers in parallel, then independent loads ---------
-  const int nsp = (nb + st.blocks_per_split - 1) / st.blocks_per_split;
+  const int nsp = min(a.nsplit, nb);
   {
     const float* spb = st.split_state + (((size_t)u * st.n_splits) * H + h) * CKV_SPLIT_FLOATS;
     float mloc = ninf(), dloc = 0.f;
@@ -975,26 +978,39 @@ cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*
 // list, LRU scratch (+ page-in), pass B, combine.
 static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                                const ckv_scratch* sc, int host_max_blocks, int u0, int nu,
-                               cudaStream_t s) {
-  StepArgs a{*c, *st, *pol, PageView{}, u0};
+                               int nsplit, cudaStream_t s) {
+  StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
   // few (unit, head) CTAs (e.g. 8-way KV-head sharding): 1024 threads per head, so
   // each CTA's serial phases are shorter; otherwise 256 threads, 4 CTAs per SM
   const long long plan_u = st->plan_units > 0 ? st->plan_units : nu;
-  const bool wide = plan_u * st->n_heads <= 2 * 148 && nbh <= 1024 * 8;
-  if (wide)
-    k_select<8, 1024><<<dim3(st->n_heads, nu), 1024, smS, s>>>(a);
-  else if (nbh <= SEL_THREADS * 8)
-    k_select<8, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
-  else if (nbh <= SEL_THREADS * 16)
-    k_select<16, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
-  else if (nbh <= SEL_THREADS * 32)
-    k_select<32, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
-  else if (nbh <= SEL_THREADS * 64)
-    k_select<64, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
-  else
-    k_select<128, SEL_THREADS><<<dim3(st->n_heads, nu), SEL_THREADS, smS, s>>>(a);
+  // variant: keys per thread x threads per (unit, head) CTA.  Few CTAs (e.g. 8-way
+  // KV-head sharding): 1024 threads, so the serial phases of each CTA are short;
+  // many: 256 threads and 4 CTAs per SM up to 8192 blocks, 512 threads beyond
+  // (more keys per thread would spill)
+  int kpt, nt;
+  if (knobs().sel_kpt > 0) {
+    kpt = knobs().sel_kpt;
+    nt = knobs().sel_nt;
+  } else if (plan_u * st->n_heads <= 2 * 148) {
+    nt = 1024;
+    kpt = nbh <= 1024 * 8 ? 8 : (nbh <= 1024 * 16 ? 16 : 32);
+  } else if (nbh <= SEL_THREADS * 32) {
+    nt = SEL_THREADS;
+    kpt = nbh <= SEL_THREADS * 8 ? 8 : (nbh <= SEL_THREADS * 16 ? 16 : 32);
+  } else {
+    nt = 512;
+    kpt = nbh <= 512 * 32 ? 32 : 64;
+  }
+  const dim3 gs(st->n_heads, nu);
+#define SEL_CASE(K, T) \
+  if (kpt == K && nt == T) k_select<K, T><<<gs, T, smS, s>>>(a); else
+  SEL_CASE(8, 1024) SEL_CASE(16, 1024) SEL_CASE(32, 1024)
+  SEL_CASE(8, 256) SEL_CASE(16, 256) SEL_CASE(32, 256) SEL_CASE(64, 256) SEL_CASE(128, 256)
+  SEL_CASE(16, 512) SEL_CASE(32, 512) SEL_CASE(64, 512)
+  return cudaErrorInvalidConfiguration;
+#undef SEL_CASE
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1045,6 +1061,31 @@ static int decode_chunks(int n_units) {
   return max(1, min(n, n_units));
 }
 
+// Pass-A splits per unit: a balanced partition of the unit's blocks whose CTA
+// count (units x splits) fills the SMs' pass-A slots in whole waves -- a last
+// wave that is half empty costs up to 1 / (2 x waves) of the stream (14% at 32
+// units x 128K).  Splits of 64..512 blocks; the fewest splits of <= 256 blocks
+// that keep >= 97% of the slots busy, else the best-filled count.
+static int pa_splits(long long units, int nb, int cap, int sms) {
+  if (nb <= 0) return 1;
+  const long long slots = (long long)sms * PA_MINB;
+  const int lo = max(1, (nb + 511) / 512), base = max(1, (nb + 255) / 256);
+  const int hi = max(1, min(cap, (nb + 63) / 64));
+  int best = min(base, hi);
+  double best_eff = -1.0;
+  for (int s = lo; s <= hi; ++s) {
+    const long long ctas = units * s;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (s >= base && eff >= 0.97) return s;
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                           const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
   g_launches = 0;
@@ -1053,16 +1094,23 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   {
     const int smS = (int)(sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4);
     set_max_dyn_smem(k_select<8, 1024>, smS);
+    set_max_dyn_smem(k_select<16, 1024>, smS);
+    set_max_dyn_smem(k_select<32, 1024>, smS);
     set_max_dyn_smem(k_select<8, SEL_THREADS>, smS);
     set_max_dyn_smem(k_select<16, SEL_THREADS>, smS);
     set_max_dyn_smem(k_select<32, SEL_THREADS>, smS);
     set_max_dyn_smem(k_select<64, SEL_THREADS>, smS);
     set_max_dyn_smem(k_select<128, SEL_THREADS>, smS);
+    set_max_dyn_smem(k_select<16, 512>, smS);
+    set_max_dyn_smem(k_select<32, 512>, smS);
+    set_max_dyn_smem(k_select<64, 512>, smS);
   }
   const int U = c->n_units;
   const int nch = decode_chunks(U);
   const int per = (U + nch - 1) / nch;
-  const int nsplit_used = (host_max_blocks + st->blocks_per_split - 1) / st->blocks_per_split;
+  const int nsplit = pa_splits(st->plan_units > 0 ? st->plan_units : U, host_max_blocks, st->n_splits,
+                               dev_state().sms);
+  const int nsplit_used = min(nsplit, host_max_blocks);
   cudaStream_t s2 = (nch > 1) ? dev_state().tail : s;
   cudaError_t e = cudaSuccess;
   if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
@@ -1071,7 +1119,7 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   for (int k = 0; k < nch; ++k) {
     const int u0 = k * per, nu = min(per, U - u0);
     if (nu <= 0) break;
-    StepArgs a{*c, *st, *pol, PageView{}, u0};
+    StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
     if (nsplit_used > 0) {
       k_pass_a<<<dim3(nsplit_used, nu), PA_WARPS * 32, smA, s>>>(a);
       ++g_launches;
@@ -1085,7 +1133,7 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
       cudaStreamWaitEvent(s2, evs[nev], 0);
       ++nev;
     }
-    e = launch_tail(c, pol, st, sc, host_max_blocks, u0, nu, s2);
+    e = launch_tail(c, pol, st, sc, host_max_blocks, u0, nu, nsplit, s2);
     if (e != cudaSuccess) break;
   }
   if (nch > 1) {

@@ -49,6 +49,7 @@ struct StepArgs {
   PageView pv;
   int32_t u0;  // first unit of this launch (units u0 + blockIdx)
   int32_t nu;  // units in this launch (persistent kernels)
+  int32_t nsplit;  // pass-A splits per unit of this step (<= st.n_splits, pa_splits())
 };
 
 // Exponent S of the unit's value scaling: every fp16 product p' * scale with

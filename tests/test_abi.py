@@ -49,7 +49,7 @@ def test_plan_host_only(lib):
     pol = PolicyConfig(exploration_rate=0.0).to_c()
     st = _lib.CkvStep()
     assert lib.ckv_plan(256, 8192, 4, ctypes.byref(pol), ctypes.byref(st)) == 0
-    assert st.blocks_per_split == 256 and st.n_splits == 32
+    assert st.blocks_per_split == 64 and st.n_splits == 128
     assert st.kcap >= 2 * 128 + 1 and st.wcap == st.kcap + 8192
     bad = PolicyConfig(exploration_rate=0.0, k_max=600).to_c()
     assert lib.ckv_plan(1, 64, 4, ctypes.byref(bad), ctypes.byref(st)) == 1
