@@ -267,7 +267,7 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
     if args.kv_heads % world:
         raise SystemExit("kv_heads must be divisible by the number of GPUs")
     U = total_units // world
-    max_tokens = args.ctx + 2 * (K + W) + max(K, 40) + 64  # timed + e2e appends
+    max_tokens = args.ctx + 3 * K + 2 * W + max(K, 40) + 64  # timed + pass-A + e2e appends
     cache = ck.DeviceKVCache(U, max_tokens, device=dev, tier2=args.tier2)
     g = torch.Generator(device=dev).manual_seed(1000 + rank)
     chunk = max(16, min(4096, (1 << 22) // U))
@@ -386,17 +386,29 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
         dist.barrier()
     t_start.record()
     for i in range(K):
-        one_step(W + i, ev_a[i])
+        one_step(W + i)
     t_end.record()
     torch.cuda.synchronize()
     collect()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end) / K
-    pa_ms = sum(a.elapsed_time(b) for a, b in ev_a) / K
     clocks = sampler.stop() if sampler else None
     n_launch = launches["n"]
     n_dense = dense_heads["n"]
+    # pass A's own duration (the roofline kernel), from CUDA events the library
+    # records around its launch on the step's stream -- in K further steps, since
+    # an event between pass A and the selection stops the selection's programmatic
+    # launch from overlapping pass A's last wave
+    saved = dict(stats), launches["n"], dense_heads["n"]
+    for i in range(K):
+        one_step(W + i, ev_a[i])
+    torch.cuda.synchronize()
+    collect()
+    stats.clear()
+    stats.update(saved[0])
+    launches["n"], dense_heads["n"] = saved[1], saved[2]
+    pa_ms = sum(a.elapsed_time(b) for a, b in ev_a) / K
     if world > 1:
         t = torch.tensor([ms, pa_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -194,6 +194,10 @@ typedef struct {
                                NULL: explore_n / explore_pos hold host-drawn samples */
   double explore_rate;      /* exploration_rate of the policy (device draws) */
   int32_t* explore_work;    /* [CKV_EXPLORE_WORK(n_units * n_heads)] device-draw scratch */
+  int32_t* flow;            /* [5][n_units] zero-initialised, self-maintaining: per-unit
+                               completion epochs of pass A / selection / pass B, so those
+                               kernels run as programmatic dependent launches that overlap
+                               on finished units (NULL: plain stream order) */
 } ckv_step;
 
 #define CKV_EXPLORE_WORK(items) (4 * (items) + 64)

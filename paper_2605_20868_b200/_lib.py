@@ -66,7 +66,8 @@ class CkvStep(ctypes.Structure):
                 ("group_flags", P), ("n_groups", I32), ("unit_done", P),
                 ("queue", P), ("stash", P), ("stash_epoch", P), ("epoch", I32),
                 ("stash_margin", ctypes.c_float), ("plan_units", I32), ("dense_splits", I32),
-                ("explore_rng", P), ("explore_rate", ctypes.c_double), ("explore_work", P)]
+                ("explore_rng", P), ("explore_rate", ctypes.c_double), ("explore_work", P),
+                ("flow", P)]
 
 
 class CkvScratch(ctypes.Structure):

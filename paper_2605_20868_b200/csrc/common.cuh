@@ -1,6 +1,7 @@
 // Shared device helpers and the Tier-1 block record layout.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -111,6 +112,24 @@ inline cudaError_t set_max_dyn_smem(F* fn, int bytes) {
   return set_max_dyn_smem_fn(reinterpret_cast<const void*>(fn), bytes);
 }
 constexpr size_t kLruSmemMax = 227 * 1024;
+// kernel launch, optionally as a programmatic dependent launch of the previous
+// kernel in the stream (see the dataflow helpers below)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 extern thread_local int g_launches;  // kernels launched by the last C-ABI call of this thread
 
 // LRU ring size for a scratch of `cap` blocks (0 = no eviction possible); see scratch.cu
@@ -246,6 +265,59 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// ---- kernel dataflow within a step (programmatic dependent launch) ----------
+// pass A -> selection -> pass B -> combine run as a chain of PDL launches: each
+// kernel lets its dependent launch as its own last CTAs start, and a consumer
+// CTA waits for its unit's producer epoch instead of the whole producer grid,
+// so the next kernel's work on finished units overlaps the producer's last wave.
+// ckv_step.flow: [5][n_units] = pass-A count, pass-A done, selection done,
+// pass-B count, pass-B done (epochs; counts reset themselves).
+enum { FLOW_PA_CNT = 0, FLOW_PA_DONE = 1, FLOW_SEL_DONE = 2, FLOW_PB_CNT = 3, FLOW_PB_DONE = 4 };
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+// every thread of the CTA returns once *flag == epoch, with acquire semantics; a
+// producer that never publishes (a launch-shape bug) traps after 2 s instead of
+// hanging the GPU
+__device__ __forceinline__ void flow_wait(const int32_t* flag, int epoch) {
+  if (threadIdx.x == 0) {
+    int ns = 64;
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_gpu(flag) != epoch) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+      if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+  (void)ld_acquire_gpu(flag);
+}
+// the CTA's writes are done: count it; the last of `total` CTAs publishes epoch
+__device__ __forceinline__ void flow_arrive(int32_t* cnt, int32_t* done, int total, int epoch) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(cnt, 1) == total - 1) {
+      *cnt = 0;
+      __threadfence();
+      st_release_gpu(done, epoch);
+    }
   }
 }
 

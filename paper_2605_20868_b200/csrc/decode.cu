@@ -111,9 +111,15 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
   const int nb = c.n_blocks[u];
+  pdl_trigger();  // the selection may launch as this grid's last CTAs start
+  int32_t* flow_cnt = st.flow ? st.flow + FLOW_PA_CNT * c.n_units + u : nullptr;
+  int32_t* flow_done = st.flow ? st.flow + FLOW_PA_DONE * c.n_units + u : nullptr;
   // balanced partition of the unit's blocks over its splits (pa_splits)
   const int nsp = min(a.nsplit, nb);
-  if (sp >= nsp) return;
+  if (sp >= nsp) {
+    if (flow_cnt) flow_arrive(flow_cnt, flow_done, gridDim.x, st.epoch);
+    return;
+  }
   const int b0 = (int)((long long)sp * nb / nsp);
   const int b1 = (int)((long long)(sp + 1) * nb / nsp);
 
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     outp[4 + ch] = O;
   }
   }
+  if (flow_cnt) flow_arrive(flow_cnt, flow_done, gridDim.x, st.epoch);
 }
 
 // =============================================================================
@@ -421,6 +428,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
   const size_t hu = (size_t)u * nh + h;
   const float* lm = st.lm1 + hu * c.max_blocks;
   HeadState& hs = *reinterpret_cast<HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
+  pdl_trigger();
+  if (st.flow) flow_wait(st.flow + FLOW_PA_DONE * c.n_units + u, st.epoch);  // this unit's pass A
 
   // the eta annotations (tail pass) and this head's pass-A split states (merge) are
   // needed later: start pulling them into L2 now
@@ -434,7 +443,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
 #define BJ(j) (tid + NT * (j))
   uint32_t kk[KPT];
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) kk[j] = (BJ(j) < nb) ? okey(__ldg(lm + BJ(j))) : 0u;
+  for (int j = 0; j < KPT; ++j) kk[j] = (BJ(j) < nb) ? okey(__ldcg(lm + BJ(j))) : 0u;
 
   if (tid < D) S.qv[tid] = (float)(st.q[hu * D + tid] * 0.08838834764831845);
   for (int i = tid; i < (c.max_blocks + 31) / 32; i += NT) fmask[i] = 0u;
@@ -919,6 +928,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
     __syncthreads();
     if (last) build_union(c, st, u, reinterpret_cast<uint32_t*>(&S), S.wsum);
     if (last) SELPROF(9);
+    if (last && st.flow) {  // the unit's selection and union list are published
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_gpu(st.flow + FLOW_SEL_DONE * c.n_units + u, st.epoch);
+    }
   }
 }
 
@@ -971,8 +985,16 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // =============================================================================
 cudaError_t launch_union(const ckv_cache*, const ckv_policy*, const ckv_step*, int, int, cudaStream_t);
 cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&, int, int,
-                         cudaStream_t);
+                         bool, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, int, cudaStream_t);
+
+// a scratch that holds every block and has no HBM slots needs no separate LRU
+// pass: pass B decides hit / miss per union item (same counts as k_lru_fast)
+static bool lru_fused(const ckv_cache* c, const ckv_scratch* sc) {
+  return lru_ring(c->max_blocks, sc->key_capacity) == 0 && lru_ring(c->max_blocks, sc->value_capacity) == 0 &&
+         sc->key_capacity > 0 && sc->value_capacity > 0 && !sc->key_slots && !sc->value_slots &&
+         !knobs().separate_lru;
+}
 
 // Everything after pass A for units [u0, u0 + nu): selection, the union work
 // list, LRU scratch (+ page-in), pass B, combine.
@@ -1004,13 +1026,15 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
     kpt = nbh <= 512 * 32 ? 32 : 64;
   }
   const dim3 gs(st->n_heads, nu);
+  const bool pdl = st->flow != nullptr;  // overlaps pass A's last wave (flow_wait per unit)
+  cudaError_t le = cudaErrorInvalidConfiguration;
 #define SEL_CASE(K, T) \
-  if (kpt == K && nt == T) k_select<K, T><<<gs, T, smS, s>>>(a); else
+  if (kpt == K && nt == T) le = launch_k(pdl, k_select<K, T>, gs, dim3(T), smS, s, a); else
   SEL_CASE(8, 1024) SEL_CASE(16, 1024) SEL_CASE(32, 1024)
   SEL_CASE(8, 256) SEL_CASE(16, 256) SEL_CASE(32, 256) SEL_CASE(64, 256) SEL_CASE(128, 256)
-  SEL_CASE(16, 512) SEL_CASE(32, 512) SEL_CASE(64, 512)
-  return cudaErrorInvalidConfiguration;
+  SEL_CASE(16, 512) SEL_CASE(32, 512) SEL_CASE(64, 512) {}
 #undef SEL_CASE
+  if (le != cudaSuccess) return le;
   ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -1019,15 +1043,11 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
     if (e != cudaSuccess) return e;
   }
   PageView pv{};
+  bool pdl_b = st->unit_done != nullptr;  // pass B directly behind the selection
   if (sc) {
-    // a scratch that holds every block and has no HBM slots needs no separate
-    // LRU pass: pass B decides hit / miss per union item (same counts as k_lru_fast)
-    const bool fuse = lru_ring(c->max_blocks, sc->key_capacity) == 0 &&
-                      lru_ring(c->max_blocks, sc->value_capacity) == 0 && sc->key_capacity > 0 &&
-                      sc->value_capacity > 0 && !sc->key_slots && !sc->value_slots &&
-                      !knobs().separate_lru;
-    if (fuse) {
-      cudaMemsetAsync(st->page_stats + (size_t)u0 * 4, 0, sizeof(int32_t) * 4 * nu, s);
+    const bool fuse = lru_fused(c, sc);
+    pdl_b = pdl_b && fuse;
+    if (fuse) {  // page_stats zeroed before pass A (launch_decode)
       pv.fused = 1;
       pv.klru = sc->key_lru;
       pv.vlru = sc->value_lru;
@@ -1046,7 +1066,7 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
     pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
     pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
   }
-  return launch_passb(c, pol, st, pv, u0, nu, s);
+  return launch_passb(c, pol, st, pv, u0, nu, pdl_b, s);
 }
 
 // Optional unit chunks (CKV_CHUNKS=n): pass A of chunk k+1 runs while the
@@ -1113,6 +1133,13 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   const int nsplit_used = min(nsplit, host_max_blocks);
   cudaStream_t s2 = (nch > 1) ? dev_state().tail : s;
   cudaError_t e = cudaSuccess;
+  if (sc && lru_fused(c, sc))
+    cudaMemsetAsync(st->page_stats, 0, sizeof(int32_t) * 4 * (size_t)U, s);
+  // the kernel dataflow needs the selection to build the union list and one
+  // unit chunk per step (the chunked overlap puts events between the kernels)
+  ckv_step stf = *st;
+  if (nch > 1 || !st->unit_done || st->queue) stf.flow = nullptr;
+  st = &stf;
   if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
   cudaEvent_t evs[64];
   int nev = 0;
@@ -1120,8 +1147,8 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
     const int u0 = k * per, nu = min(per, U - u0);
     if (nu <= 0) break;
     StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
-    if (nsplit_used > 0) {
-      k_pass_a<<<dim3(nsplit_used, nu), PA_WARPS * 32, smA, s>>>(a);
+    if (nsplit_used > 0 || st->flow) {  // with the dataflow every unit's pass A must publish
+      k_pass_a<<<dim3(max(nsplit_used, 1), nu), PA_WARPS * 32, smA, s>>>(a);
       ++g_launches;
     }
     if (k == nch - 1 || u0 + nu >= U) {

@@ -479,7 +479,14 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   const int C = st.n_chunks;
   int kb = 0;
   if (!st.queue) {
-    pass_b_chunk<SLOTS>(a, S, a.u0 + blockIdx.y, blockIdx.x, C, kb);
+    const int u = a.u0 + blockIdx.y;
+    const int U = a.c.n_units;
+    if (st.flow) {
+      pdl_trigger();
+      flow_wait(st.flow + FLOW_SEL_DONE * U + u, st.epoch);  // this unit's selection + union
+    }
+    pass_b_chunk<SLOTS>(a, S, u, blockIdx.x, C, kb);
+    if (st.flow) flow_arrive(st.flow + FLOW_PB_CNT * U + u, st.flow + FLOW_PB_DONE * U + u, gridDim.x, st.epoch);
     return;
   }
   __shared__ int s_item;
@@ -508,6 +515,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   const ckv_step& st = a.st;
   const ckv_policy& pol = a.pol;
   const int h = blockIdx.x, u = a.u0 + blockIdx.y, tid = threadIdx.x;
+  if (st.flow && !st.queue) flow_wait(st.flow + FLOW_PB_DONE * c.n_units + u, st.epoch);  // its pass B
   const int nh = st.n_heads;
   const size_t hu = (size_t)u * nh + h;
   const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
@@ -749,9 +757,12 @@ cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_st
 }
 
 cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                         const PageView& pv, int u0, int nu, cudaStream_t s) {
+                         const PageView& pv, int u0, int nu, bool pdl, cudaStream_t s) {
   passb_attrs(c);
   StepArgs a{*c, *st, *pol, pv, u0, nu};
+  // the dataflow chain (st->flow): pass B right behind the selection, combine
+  // right behind pass B, each waiting per unit (no persistent queue in that mode)
+  const bool flow = st->flow != nullptr && !st->queue;
   const bool slots_ = pv.kslots || pv.vslots;
   if (st->queue) {
     DevState& ds = dev_state();
@@ -765,11 +776,14 @@ cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_st
     if (slots_) k_pass_b<true><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
     else k_pass_b<false><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
   } else {
-    if (slots_) k_pass_b<true><<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
-    else k_pass_b<false><<<dim3(st->n_chunks, nu), PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
+    const dim3 g(st->n_chunks, nu);
+    cudaError_t e = slots_ ? launch_k(pdl && flow, k_pass_b<true>, g, dim3(PB_WARPS * 32), sizeof(PassBSmem), s, a)
+                           : launch_k(pdl && flow, k_pass_b<false>, g, dim3(PB_WARPS * 32), sizeof(PassBSmem), s, a);
+    if (e != cudaSuccess) return e;
   }
-  k_combine<<<dim3(st->n_heads, nu), 128, 0, s>>>(a);
+  cudaError_t e = launch_k(flow, k_combine, dim3(st->n_heads, nu), dim3(128), 0, s, a);
   g_launches += 2;
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -151,6 +151,11 @@ class CertifiedDecoder:
             setattr(st, name, _ptr(t))
         if os.environ.get("CKV_SEPARATE_UNION"):  # A/B knob: union list by its own launch
             st.unit_done = None
+        # per-unit completion epochs: pass A -> selection -> pass B -> combine run as
+        # programmatic dependent launches that overlap on finished units
+        self.flow = torch.zeros((5 * U,), dtype=torch.int32, device=dev)
+        if not os.environ.get("CKV_NO_FLOW"):
+            st.flow = _ptr(self.flow)
         # phase-1 score stash: pass A keeps the quantized scores of blocks likely to be
         # promoted (predicted from the previous step's tail threshold) so pass B needs
         # only the value part of their Tier-1 record (exact either way)
