@@ -194,11 +194,27 @@ typedef struct {
                                NULL: explore_n / explore_pos hold host-drawn samples */
   double explore_rate;      /* exploration_rate of the policy (device draws) */
   int32_t* explore_work;    /* [CKV_EXPLORE_WORK(n_units * n_heads)] device-draw scratch */
-  int32_t* flow;            /* [5][n_units] zero-initialised, self-maintaining: per-unit
-                               completion epochs of pass A / selection / pass B, so those
-                               kernels run as programmatic dependent launches that overlap
-                               on finished units (NULL: plain stream order) */
+  int32_t* flow;            /* [6 * n_units + 4] zero-initialised, self-maintaining: per-unit
+                               completion epochs of pass A / selection / pass B (+ counters
+                               and step-wide words), so those kernels, and in ckv_decode_step
+                               the dense pass, run as programmatic dependent launches that
+                               overlap on finished units (NULL: plain stream order) */
+  unsigned long long* trace; /* [32][2] optional timeline (profiling): per kernel of the step,
+                               the first CTA start / last CTA end (globaltimer ns) by
+                               atomicMin / atomicMax; the caller resets it (NULL: off) */
 } ckv_step;
+
+/* trace slots */
+#define CKV_TR_PASS_A 0
+#define CKV_TR_SELECT 1
+#define CKV_TR_PASS_B 2
+#define CKV_TR_COMBINE 3
+#define CKV_TR_FLAGS 4
+#define CKV_TR_RESOLVE 5
+#define CKV_TR_DENSE 6
+#define CKV_TR_XDRAW 7
+#define CKV_TR_EXPLORE 8
+#define CKV_TR_LRU 9
 
 #define CKV_EXPLORE_WORK(items) (4 * (items) + 64)
 

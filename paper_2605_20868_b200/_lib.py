@@ -67,7 +67,7 @@ class CkvStep(ctypes.Structure):
                 ("queue", P), ("stash", P), ("stash_epoch", P), ("epoch", I32),
                 ("stash_margin", ctypes.c_float), ("plan_units", I32), ("dense_splits", I32),
                 ("explore_rng", P), ("explore_rate", ctypes.c_double), ("explore_work", P),
-                ("flow", P)]
+                ("flow", P), ("trace", P)]
 
 
 class CkvScratch(ctypes.Structure):

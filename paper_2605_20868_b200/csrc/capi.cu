@@ -65,9 +65,10 @@ cudaError_t launch_fault_offset(const ckv_cache*, int, int, int, float, cudaStre
 cudaError_t launch_tier2_drop(const ckv_cache*, int, int, cudaStream_t);
 cudaError_t launch_f64_to_f16(const double*, uint16_t*, size_t, cudaStream_t);
 cudaError_t launch_reset(const ckv_cache*, cudaStream_t);
-cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, const ckv_scratch*, int,
+cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, const ckv_scratch*, int, bool,
                           cudaStream_t);
-cudaError_t launch_dense(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, cudaStream_t);
+cudaError_t launch_dense(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, bool, cudaStream_t);
+bool decode_flow(const ckv_cache*, const ckv_step*);
 cudaError_t launch_group_flags(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_explore_draw(const ckv_cache*, const ckv_step*, cudaStream_t);
@@ -177,15 +178,21 @@ static bool step_ok(const ckv_cache* c, const ckv_policy* pol, const ckv_step* s
   return host_max_blocks >= 0 && host_max_blocks <= c->max_blocks;
 }
 
-ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
-                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+static ckv_status decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                               const ckv_scratch* scratch, int32_t host_max_blocks, bool finish,
+                               void* stream) {
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   if (scratch && (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters))
     return CKV_EINVAL;
   // Tier-2 loss is reported per step
   cudaError_t e = cudaMemsetAsync(c->status + CKV_ST_TIER2, 0, sizeof(int32_t), S(stream));
   if (e != cudaSuccess) return st_of(e);
-  return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, S(stream)));
+  return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, finish, S(stream)));
+}
+
+ckv_status ckv_decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
+                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+  return decode_begin(c, pol, st, scratch, host_max_blocks, false, stream);
 }
 
 ckv_status ckv_decode_flags(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
@@ -212,7 +219,7 @@ ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, const ckv_scratch
   ckv_policy dummy{};
   dummy.k_max = 1;
   if (!step_ok(c, &dummy, st, host_max_blocks)) return CKV_EINVAL;
-  return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, S(stream)));
+  return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, false, S(stream)));
 }
 
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
@@ -224,6 +231,13 @@ ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* s
 
 ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
                            const ckv_scratch* scratch, int32_t host_max_blocks, void* stream) {
+  if (st && c && !st->explore_rng && ckv::decode_flow(c, st)) {
+    // the whole step as one dataflow: the last combine CTA resolves the step-wide
+    // Rung 4 and the dense list, the dense pass launches right behind it
+    ckv_status r = decode_begin(c, pol, st, scratch, host_max_blocks, true, stream);
+    if (r != CKV_OK) return r;
+    return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, true, S(stream)));
+  }
   ckv_status r = ckv_decode_begin(c, pol, st, scratch, host_max_blocks, stream);
   if (r != CKV_OK) return r;
   int32_t* en = st->explore_n;

@@ -273,9 +273,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // kernel lets its dependent launch as its own last CTAs start, and a consumer
 // CTA waits for its unit's producer epoch instead of the whole producer grid,
 // so the next kernel's work on finished units overlaps the producer's last wave.
-// ckv_step.flow: [5][n_units] = pass-A count, pass-A done, selection done,
-// pass-B count, pass-B done (epochs; counts reset themselves).
-enum { FLOW_PA_CNT = 0, FLOW_PA_DONE = 1, FLOW_SEL_DONE = 2, FLOW_PB_CNT = 3, FLOW_PB_DONE = 4 };
+// ckv_step.flow: [6][n_units] = pass-A count, pass-A done, selection done,
+// pass-B count, pass-B done, combine count (epochs; counts reset themselves),
+// then FLOW_STEP_WORDS step-wide words.
+enum { FLOW_PA_CNT = 0, FLOW_PA_DONE = 1, FLOW_SEL_DONE = 2, FLOW_PB_CNT = 3, FLOW_PB_DONE = 4,
+       FLOW_CB_UNIT = 5, FLOW_UNIT_WORDS = 6 };
+// step-wide words behind the per-unit ones: combine CTAs done, step resolved,
+// dense units listed so far, some head requested Rung 4
+enum { FLOW_CB_CNT = 0, FLOW_RESOLVED = 1, FLOW_DENSE_N = 2, FLOW_ANY4 = 3, FLOW_STEP_WORDS = 4 };
+__host__ __device__ inline int32_t* flow_step(int32_t* flow, int n_units, int k) {
+  return flow + FLOW_UNIT_WORDS * n_units + k;
+}
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
@@ -320,6 +328,18 @@ __device__ __forceinline__ void flow_arrive(int32_t* cnt, int32_t* done, int tot
     }
   }
 }
+
+// per-kernel first-start / last-end stamps (ckv_step.trace, profiling only)
+struct TraceScope {
+  unsigned long long* slot;
+  __device__ __forceinline__ TraceScope(unsigned long long* tr, int id)
+      : slot(tr ? tr + 2 * id : nullptr) {
+    if (slot && threadIdx.x == 0) atomicMin(slot, globaltimer_ns());
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    if (slot && threadIdx.x == 0) atomicMax(slot + 1, globaltimer_ns());
+  }
+};
 
 // L2 prefetch of a global range by the TMA unit (no registers, no shared memory)
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_PASS_A);
   const int u = a.u0 + blockIdx.y, sp = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nh = st.n_heads;
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
   uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_SELECT);
   const ckv_policy& pol = a.pol;
   const int h = blockIdx.x, u = a.u0 + blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -985,7 +987,7 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
 // =============================================================================
 cudaError_t launch_union(const ckv_cache*, const ckv_policy*, const ckv_step*, int, int, cudaStream_t);
 cudaError_t launch_passb(const ckv_cache*, const ckv_policy*, const ckv_step*, const PageView&, int, int,
-                         bool, cudaStream_t);
+                         bool, bool, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, int, cudaStream_t);
 
 // a scratch that holds every block and has no HBM slots needs no separate LRU
@@ -1000,7 +1002,7 @@ static bool lru_fused(const ckv_cache* c, const ckv_scratch* sc) {
 // list, LRU scratch (+ page-in), pass B, combine.
 static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                                const ckv_scratch* sc, int host_max_blocks, int u0, int nu,
-                               int nsplit, cudaStream_t s) {
+                               int nsplit, bool finish, cudaStream_t s) {
   StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
   const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
@@ -1066,7 +1068,7 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
     pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
     pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
   }
-  return launch_passb(c, pol, st, pv, u0, nu, pdl_b, s);
+  return launch_passb(c, pol, st, pv, u0, nu, pdl_b, finish, s);
 }
 
 // Optional unit chunks (CKV_CHUNKS=n): pass A of chunk k+1 runs while the
@@ -1106,8 +1108,13 @@ static int pa_splits(long long units, int nb, int cap, int sms) {
   return best;
 }
 
+// whether launch_decode runs the step as a dataflow (see flow_wait / flow_arrive)
+bool decode_flow(const ckv_cache* c, const ckv_step* st) {
+  return st->flow && st->unit_done && !st->queue && decode_chunks(c->n_units) == 1;
+}
+
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                          const ckv_scratch* sc, int host_max_blocks, cudaStream_t s) {
+                          const ckv_scratch* sc, int host_max_blocks, bool finish, cudaStream_t s) {
   g_launches = 0;
   const size_t smA = sizeof(PassASmem);
   set_max_dyn_smem(k_pass_a, (int)smA);
@@ -1138,7 +1145,7 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   // the kernel dataflow needs the selection to build the union list and one
   // unit chunk per step (the chunked overlap puts events between the kernels)
   ckv_step stf = *st;
-  if (nch > 1 || !st->unit_done || st->queue) stf.flow = nullptr;
+  if (!decode_flow(c, st)) stf.flow = nullptr;
   st = &stf;
   if (st->prof_begin) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_begin), s);
   cudaEvent_t evs[64];
@@ -1160,7 +1167,7 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
       cudaStreamWaitEvent(s2, evs[nev], 0);
       ++nev;
     }
-    e = launch_tail(c, pol, st, sc, host_max_blocks, u0, nu, nsplit, s2);
+    e = launch_tail(c, pol, st, sc, host_max_blocks, u0, nu, nsplit, finish && nch == 1, s2);
     if (e != cudaSuccess) break;
   }
   if (nch > 1) {

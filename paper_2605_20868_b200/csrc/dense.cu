@@ -15,14 +15,14 @@ namespace ckv {
 
 constexpr int DN_MAXSPLIT = 256;  // splits per dense unit (merge buffer)
 #ifndef DN_SPLITS
-#define DN_SPLITS 128
+#define DN_SPLITS 256
 #endif
 constexpr int DN_WARPS = 4;
 
 struct DenseArgs {
   ckv_cache c;
   ckv_step st;
-  int32_t group;     // (unused)
+  int32_t resolved;  // the step was resolved by the last combine CTA: wait for its epoch
   int32_t n_dsplit;  // splits per dense unit of this launch (set on device from the count)
   int32_t blk_per_split;  // (unused)
   PageView pv;  // HBM scratch slots (Tier-2 in host RAM): resident blocks are read from HBM
@@ -30,13 +30,11 @@ struct DenseArgs {
 
 __device__ __forceinline__ float dninf() { return __int_as_float(0xff800000); }
 
-__device__ __forceinline__ int rung4_group_of(const ckv_step& st, int u) {
-  return st.unit_group ? st.unit_group[u] : u / st.rung4_group;
-}
 
 // every head whose certificate requests Rung 4 flags its unit's group
 __global__ void k_group_flags(DenseArgs a) {
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_FLAGS);
   const int nh = st.n_heads;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.c.n_units * nh) return;
@@ -49,6 +47,7 @@ __global__ void k_group_flags(DenseArgs a) {
 // a flagged group returns dense for all its heads; list the units needing a dense pass
 __global__ void k_resolve(DenseArgs a) {
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_RESOLVE);
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= a.c.n_units) return;
   const int nh = st.n_heads;
@@ -156,6 +155,8 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   DenseArgs a = a_in;
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_DENSE);
+  if (a.resolved) flow_wait(flow_step(st.flow, c.n_units, FLOW_RESOLVED), st.epoch);
   // persistent over (item, split) tasks; the split count adapts to the number of
   // dense units so that a few of them still spread over every SM
   const int count = st.dense_list[0];
@@ -291,9 +292,9 @@ cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStrea
 }
 
 cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scratch* sc,
-                         int host_max_tokens, cudaStream_t s) {
+                         int host_max_tokens, bool resolved, cudaStream_t s) {
   (void)host_max_tokens;
-  DenseArgs a{*c, *st, 0, 1, 0, PageView{}};
+  DenseArgs a{*c, *st, resolved ? 1 : 0, 1, 0, PageView{}};
   if (sc && (sc->key_slots || sc->value_slots)) {
     a.pv.kslots = sc->key_capacity > 0 ? sc->key_slots : nullptr;
     a.pv.vslots = sc->value_capacity > 0 ? sc->value_slots : nullptr;
@@ -311,10 +312,17 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scrat
     ds.dense_slots = max(1, ds.sms * max(1, per));
   }
   const int slots = ds.dense_slots;
+  if (resolved) {  // right behind the combine that resolved the step (PDL)
+    cudaError_t e = launch_k(true, k_dense, dim3(slots), dim3(DN_WARPS * 32), 0, s, a);
+    g_launches += 1;
+    return e;
+  }
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t) * (1 + c->n_units), s);  // count + done counters
   k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
   k_dense<<<slots, DN_WARPS * 32, 0, s>>>(a);
   g_launches += 2;
+  // the dataflow path (resolved) expects the step-wide requests cleared
+  cudaMemsetAsync(st->group_flags, 0, sizeof(int32_t) * st->n_groups, s);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(XP_WARPS * 32) k_explore(StepArgs a) {
   uint32_t* fb = reinterpret_cast<uint32_t*>(smem_raw + sizeof(ExploreSmem));  // [W] promoted
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_EXPLORE);
   const ckv_policy& pol = a.pol;
   const int h = blockIdx.x, u = blockIdx.y, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;

@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(XD_MAX_WARPS * 32) k_explore_draw(DrawArgs a) 
   cg::grid_group grid = cg::this_grid();
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_XDRAW);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int gw = blockIdx.x * (blockDim.x >> 5) + wib;

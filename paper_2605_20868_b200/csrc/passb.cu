@@ -467,6 +467,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   PassBSmem& S = *reinterpret_cast<PassBSmem*>(smem_raw);
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_PASS_B);
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int w = 0; w < PB_WARPS; ++w) {
@@ -510,9 +511,63 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 3) k_pass_b(StepArgs a) {
 }
 
 // -----------------------------------------------------------------------------
+// Step-wide Rung 4 and the dense work list (k_group_flags + k_resolve in the
+// dataflow): every unit's last combine CTA lists the unit if one of its own heads
+// returns dense; the last combine CTA of the step only has work when some head
+// requested Rung 4 -- then every head of the requesting units' groups turns
+// dense (harness.py:362-372) and the list is rebuilt over all units.
+__device__ void unit_dense_item(const ckv_cache& c, const ckv_step& st, int u) {
+  const int nh = st.n_heads;
+  int mask = 0;
+  for (int h = 0; h < nh; ++h)
+    if (__ldcg(&st.cert[(size_t)u * nh + h].returned_kind) != 0) mask |= 1 << h;
+  if (mask) {
+    const int slot = atomicAdd(flow_step(st.flow, c.n_units, FLOW_DENSE_N), 1);
+    st.dense_list[1 + c.n_units + slot] = u | (mask << 24);
+  }
+}
+
+__device__ void resolve_step(const ckv_cache& c, const ckv_step& st) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nh = st.n_heads, U = c.n_units;
+  int32_t* nlist = flow_step(st.flow, U, FLOW_DENSE_N);
+  int32_t* any4 = flow_step(st.flow, U, FLOW_ANY4);
+  __shared__ int count, rung4;
+  if (tid == 0) {
+    rung4 = __ldcg(any4);
+    count = rung4 ? 0 : __ldcg(nlist);
+  }
+  __syncthreads();
+  if (rung4) {
+    for (int u = tid; u < U; u += nt) {
+      const int g = rung4_group_of(st, u);
+      const bool gf = (g >= 0 && g < st.n_groups) && __ldcg(&st.group_flags[g]) != 0;
+      int mask = 0;
+      for (int h = 0; h < nh; ++h) {
+        ckv_cert& ct = st.cert[(size_t)u * nh + h];
+        if (gf) ct.returned_kind = 2;
+        if (__ldcg(&ct.returned_kind) != 0) mask |= 1 << h;
+      }
+      if (mask) {
+        const int slot = atomicAdd(&count, 1);
+        st.dense_list[1 + U + slot] = u | (mask << 24);
+      }
+    }
+    __syncthreads();
+    for (int g = tid; g < st.n_groups; g += nt) st.group_flags[g] = 0;  // for the next step
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st.dense_list[0] = count;
+    *nlist = 0;
+    *any4 = 0;
+  }
+}
+
 __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_COMBINE);
   const ckv_policy& pol = a.pol;
   const int h = blockIdx.x, u = a.u0 + blockIdx.y, tid = threadIdx.x;
   if (st.flow && !st.queue) flow_wait(st.flow + FLOW_PB_DONE * c.n_units + u, st.epoch);  // its pass B
@@ -736,6 +791,37 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
     if (fl & (CKV_F_CANARY | CKV_F_NUMERIC)) kind = 2;
     else if (fl & (CKV_F_RANKING | CKV_F_BOUNDARY)) kind = 1;
     ct.returned_kind = kind;
+    if (a.finish && kind == 2) {  // a step-wide Rung-4 request for the unit's group
+      const int g = rung4_group_of(st, u);
+      if (g >= 0 && g < st.n_groups) atomicOr(&st.group_flags[g], 1);
+      atomicOr(flow_step(st.flow, c.n_units, FLOW_ANY4), 1);
+    }
+  }
+  if (a.finish) {  // the unit's last head lists it, the step's last CTA resolves
+    __shared__ int last_u, last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      int32_t* cu = st.flow + FLOW_CB_UNIT * c.n_units + u;
+      last_u = atomicAdd(cu, 1) == nh - 1;
+      if (last_u) {
+        *cu = 0;
+        __threadfence();
+        unit_dense_item(c, st, u);
+      }
+      int32_t* cnt = flow_step(st.flow, c.n_units, FLOW_CB_CNT);
+      __threadfence();
+      last = atomicAdd(cnt, 1) == (int)(gridDim.x * gridDim.y) - 1;
+      if (last) *cnt = 0;
+      __threadfence();
+    }
+    __syncthreads();
+    if (last) {
+      resolve_step(c, st);
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_gpu(flow_step(st.flow, c.n_units, FLOW_RESOLVED), st.epoch);
+    }
   }
 }
 
@@ -757,9 +843,9 @@ cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_st
 }
 
 cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
-                         const PageView& pv, int u0, int nu, bool pdl, cudaStream_t s) {
+                         const PageView& pv, int u0, int nu, bool pdl, bool finish, cudaStream_t s) {
   passb_attrs(c);
-  StepArgs a{*c, *st, *pol, pv, u0, nu};
+  StepArgs a{*c, *st, *pol, pv, u0, nu, 0, finish && st->flow && !st->queue ? 1 : 0};
   // the dataflow chain (st->flow): pass B right behind the selection, combine
   // right behind pass B, each waiting per unit (no persistent queue in that mode)
   const bool flow = st->flow != nullptr && !st->queue;

@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru(LruArgs a) {
   extern __shared__ __align__(16) int32_t sm[];
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_LRU);
   const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
   const int maxb = c.max_blocks;
   const int nb = c.n_blocks[u];
@@ -279,6 +280,7 @@ __global__ void __launch_bounds__(LRU_THREADS) k_lru_fast(LruArgs ka, LruArgs va
   const int kind = blockIdx.y;
   const LruArgs& a = kind ? va : ka;
   const ckv_step& st = a.st;
+  TraceScope trace_(st.trace, CKV_TR_LRU);
   const int u = a.u0 + blockIdx.x, tid = threadIdx.x;
   const int maxb = a.c.max_blocks;
   int32_t* L = a.state + (size_t)u * a.words;

@@ -50,7 +50,12 @@ struct StepArgs {
   int32_t u0;  // first unit of this launch (units u0 + blockIdx)
   int32_t nu;  // units in this launch (persistent kernels)
   int32_t nsplit;  // pass-A splits per unit of this step (<= st.n_splits, pa_splits())
+  int32_t finish;  // the last combine CTA resolves the step (group flags, dense list)
 };
+
+__device__ __forceinline__ int rung4_group_of(const ckv_step& st, int u) {
+  return st.unit_group ? st.unit_group[u] : u / st.rung4_group;
+}
 
 // Exponent S of the unit's value scaling: every fp16 product p' * scale with
 // p' = p * 2^S <= 2^S stays below 2^15 (scale <= max(2 v_max / 15, 1), since

@@ -153,7 +153,7 @@ class CertifiedDecoder:
             st.unit_done = None
         # per-unit completion epochs: pass A -> selection -> pass B -> combine run as
         # programmatic dependent launches that overlap on finished units
-        self.flow = torch.zeros((5 * U,), dtype=torch.int32, device=dev)
+        self.flow = torch.zeros((6 * U + 4,), dtype=torch.int32, device=dev)
         if not os.environ.get("CKV_NO_FLOW"):
             st.flow = _ptr(self.flow)
         # phase-1 score stash: pass A keeps the quantized scores of blocks likely to be
