@@ -146,10 +146,30 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const float* stash_u = st.stash ? st.stash + (size_t)u * c.max_blocks * 64 : nullptr;
   int le[2], lsl[2], lval[2], lsep[2], lvs[2];
   float lsm[2], let_[2];
+  // fused LRU accounting (scratch holding every block): a block's first request
+  // ever is a miss, every other a hit -- decided lane-parallel for a window of 32
+  // items when its work entries are loaded, off the item loop
+  int lk_h = 0, lk_m = 0, lv_h = 0, lv_m = 0, req_k = 0, req_v = 0;
   auto load_e = [&](int s, int kbase) {
     const int it = item_at(kbase + lane);
     const int e2 = (it >= 0) ? work[it] : -1;
     if (s) le[1] = e2; else le[0] = e2;
+    if (pv.fused && e2 != -1) {
+      const int b2 = e2 & 0xffffff;
+      const int nk = __popc(((uint32_t)e2 >> 24) & 0xfu), nv = __popc(((uint32_t)e2 >> 28) & 0xfu);
+      if (nk) {
+        const int miss = atomicExch(pv.klru + (size_t)u * pv.kstride + 4 + b2, 1) == 0;
+        lk_m += miss;
+        lk_h += nk - miss;
+        req_k += nk;
+      }
+      if (nv) {
+        const int miss = atomicExch(pv.vlru + (size_t)u * pv.vstride + 4 + b2, 1) == 0;
+        lv_m += miss;
+        lv_h += nv - miss;
+        req_v += nv;
+      }
+    }
   };
   auto load_words = [&](int s) {
     const int e2 = s ? le[1] : le[0];
@@ -220,17 +240,9 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     fence_proxy_async();
     issue(mc, kb & 1);
   }
-  // fused LRU accounting (lane 0): hits / misses of this warp's items; the
-  // stamp exchange of item k is folded in at item k+1 (its latency off the path)
-  int lk_h = 0, lk_m = 0, lv_h = 0, lv_m = 0, req_k = 0, req_v = 0;
-  int pend_k = 1, pend_v = 1, pend_nk = 0, pend_nv = 0;
-  auto fold_lru = [&]() {
-    lk_m += (pend_nk > 0 && pend_k == 0);
-    lk_h += pend_nk - (pend_nk > 0 && pend_k == 0);
-    lv_m += (pend_nv > 0 && pend_v == 0);
-    lv_h += pend_nv - (pend_nv > 0 && pend_v == 0);
-    pend_nk = pend_nv = 0;
-  };
+  // the item two ahead, advanced incrementally (no division in the loop)
+  const int per_chunk = (IPC + PB_WARPS - 1 - warp) / PB_WARPS;
+  int nx_chunk = (per_chunk > 2) ? 0 : 2 / per_chunk, nx_within = (per_chunk > 2) ? 2 : 2 % per_chunk;
   int k = 0;
   for (; cur >= 0; ++k) {
     const int stg = (kb + k) & 1;
@@ -247,15 +259,6 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     const uint32_t fm = ((uint32_t)e >> 24) & 0xfu, vm = ((uint32_t)e >> 28) & 0xfu;
     const bool inF = (fm >> h) & 1u, inV = (vm >> h) & 1u;
     if ((fm | vm) && lane == 0 && !mc.valid) atomicOr(&c.status[CKV_ST_TIER2], 1);
-    if (pv.fused && lane == 0) {
-      fold_lru();
-      pend_nk = __popc(fm);
-      pend_nv = __popc(vm);
-      req_k += pend_nk;
-      req_v += pend_nv;
-      if (pend_nk) pend_k = atomicExch(pv.klru + (size_t)u * pv.kstride + 4 + b, 1);
-      if (pend_nv) pend_v = atomicExch(pv.vlru + (size_t)u * pv.vstride + 4 + b, 1);
-    }
     const float smax = mc.smax;
     const float eta_b = mc.eta;
     mbar_wait(&S.bar[warp][stg], (uint32_t)((kb + k) >> 1) & 1u);
@@ -379,14 +382,32 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     }
     __syncwarp();
     cur = nxt;
-    i1 = item_at(k + 2);
+    {  // item k + 2
+      const int idx = (ck + nx_chunk * C) * IPC + warp + nx_within * PB_WARPS;
+      const int cend = min(nwork, (ck + nx_chunk * C) * IPC + IPC);
+      i1 = (idx < cend) ? idx : -1;
+      if (++nx_within == per_chunk) {
+        nx_within = 0;
+        ++nx_chunk;
+      }
+    }
     mc = mn;
     mn = fetch(k + 2);
   }
   kb += k;
   if (SLOTS && lane == 0 && pv.kslots) bulk_wait_all();  // slot fills done before the stages are reused / exit
+  if (pv.fused) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lk_h += __shfl_xor_sync(0xffffffffu, lk_h, o);
+      lk_m += __shfl_xor_sync(0xffffffffu, lk_m, o);
+      lv_h += __shfl_xor_sync(0xffffffffu, lv_h, o);
+      lv_m += __shfl_xor_sync(0xffffffffu, lv_m, o);
+      req_k += __shfl_xor_sync(0xffffffffu, req_k, o);
+      req_v += __shfl_xor_sync(0xffffffffu, req_v, o);
+    }
+  }
   if (pv.fused && lane == 0) {
-    fold_lru();
     if (lk_h | lk_m | lv_h | lv_m) {
       atomicAdd(pv.page_stats + u * 4 + 0, lk_h);
       atomicAdd(pv.page_stats + u * 4 + 1, lk_m);
