@@ -39,19 +39,6 @@ struct PassBSmem {
   float ca[PB_WARPS][H][B];  // coefficient of the original v
 };
 
-// A operand of the INT4 codes as exact fp16 integers (1024 + u) - 1024 for
-// group g (see the record layout in common.cuh).
-__device__ __forceinline__ void vcode_a(uint32_t w, uint32_t& a0, uint32_t& a1, uint32_t& a2,
-                                        uint32_t& a3) {
-  const uint32_t magic = 0x64006400u, m1024 = 0x64006400u;
-  const uint32_t k16 = 0x2c002c00u, m64 = 0xd400d400u;  // 1/16, -64
-  const uint32_t w8 = w >> 8;
-  a0 = h2_sub((w & 0x000f000fu) | magic, m1024);
-  a1 = h2_sub((w8 & 0x000f000fu) | magic, m1024);
-  a2 = h2_fma((w & 0x00f000f0u) | magic, k16, m64);   // (1024 + 16u) / 16 - 64
-  a3 = h2_fma((w8 & 0x00f000f0u) | magic, k16, m64);
-}
-
 // One chunk (IPC consecutive items of unit u's union list, 4 warps interleaved).
 // Page one missed FP16 tile (4 KB) from Tier-2 into its HBM slot, 16 B per lane per
 // group; the caller's lane re-reads exactly the words it wrote.  Out of line: it
@@ -332,34 +319,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       accz[0] *= alpha; accz[1] *= alpha; accz[2] *= alpha; accz[3] *= alpha;
     }
     __syncwarp();
-    {  // v_hat part: B = cq' * scale per group (hi/lo), exact integer codes
-      uint32_t h01, l01, h23, l23;
-      const float4 p4 = *reinterpret_cast<const float4*>(&S.cq[warp][hb][4 * (lane & 3)]);
-      split_h2(p4.x, p4.y, h01, l01);
-      split_h2(p4.z, p4.w, h23, l23);
-      const uint32_t nph0 = lo_lane ? (h01 ^ 0x80008000u) : 0u, nph1 = lo_lane ? (h23 ^ 0x80008000u) : 0u;
-      const uint32_t plo0 = lo_lane ? l01 : 0u, plo1 = lo_lane ? l23 : 0u;
-      const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
-      const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
-      const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-      const uint4* sc = reinterpret_cast<const uint4*>(rec + OFF_VSCALE + (lane & 3) * 64);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 s4 = sc[q];
-        const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-        for (int e2 = 0; e2 < 2; ++e2) {
-          const int g = 2 * q + e2;
-          const uint32_t s01 = sv[2 * e2], s23 = sv[2 * e2 + 1];
-          const uint32_t b0 = h2_fma(plo0, s01, h2_fma(h01, s01, h2_mul(nph0, s01)));
-          const uint32_t b1 = h2_fma(plo1, s23, h2_fma(h23, s23, h2_mul(nph1, s23)));
-          uint32_t a0, a1, a2, a3;
-          vcode_a(wv[g], a0, a1, a2, a3);
-          mma_f16r(acc[g], a0, a1, a2, a3, b0, b1);
-        }
-      }
-      const uint2 oz = *reinterpret_cast<const uint2*>(rec + OFF_VOFF + ((lane & 3) * 8 + (lane >> 2)) * 8);
-      mma_f16r(accz, oz.x, 0u, oz.y, 0u, lo_lane ? l01 : h01, lo_lane ? l23 : h23);
+    {  // v_hat part, as pass A's speculative P.V: the INT4 codes as fp16 subnormals
+       // (A operand without conversion), B = cq' * scale (hi/lo); acc in units 2^-24
+      PVFrag F;
+      pv_frag(F, *reinterpret_cast<const float4*>(&S.cq[warp][hb][4 * (lane & 3)]), lo_lane);
+      pv_block_sub(acc, accz, F, rec, lane);
     }
     if (vm) {  // warp-uniform: some head of this block is value-promoted: B = ca' (hi/lo)
       uint32_t h01, l01, h23, l23;
@@ -378,7 +342,14 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
 #pragma unroll
       for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
 #pragma unroll
-      for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, b0, b1);
+      for (int g = 0; g < NG; ++g) {  // original values in units 1, acc in 2^-24: exact rescale
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        mma_f16r(t, av[g].x, av[g].y, av[g].z, av[g].w, b0, b1);
+        acc[g][0] = fmaf(t[0], 5.9604644775390625e-8f, acc[g][0]);
+        acc[g][1] = fmaf(t[1], 5.9604644775390625e-8f, acc[g][1]);
+        acc[g][2] = fmaf(t[2], 5.9604644775390625e-8f, acc[g][2]);
+        acc[g][3] = fmaf(t[3], 5.9604644775390625e-8f, acc[g][3]);
+      }
     }
     __syncwarp();
     cur = nxt;
@@ -444,8 +415,8 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   for (int g = 0; g < NG; ++g) {
     const float zg = __shfl_sync(0xffffffffu, oz, 4 * g + h);
     const int c0 = 16 * g + t0;
-    accs[(warp * H + h) * D + c0] = (acc[g][0] + acc[g][1] + zg) * inv;
-    accs[(warp * H + h) * D + c0 + 8] = (acc[g][2] + acc[g][3] + zg) * inv;
+    accs[(warp * H + h) * D + c0] = fmaf(acc[g][0] + acc[g][1], 16777216.f, zg) * inv;
+    accs[(warp * H + h) * D + c0 + 8] = fmaf(acc[g][2] + acc[g][3], 16777216.f, zg) * inv;
   }
   if (lane < H) {
     mw[(warp * H + lane) * 4 + 0] = m_h;

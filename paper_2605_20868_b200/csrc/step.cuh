@@ -147,4 +147,62 @@ __device__ inline void build_union(const ckv_cache& c, const ckv_step& st, int u
   if (tid == 0) st.n_work[u] = base;
 }
 
+// The speculative Phase-2 P.V of one block on the tensor cores.  The INT4
+// codes are fed as fp16 *subnormals* (the bit pattern of the code u is the
+// half u * 2^-24, so one AND per two codes builds the A operand, no bias);
+// B = p' * scale per (token, group) as an fp16 hi/lo pair (column 2h + part),
+// so each product is exact and the sum is fp32.  Tokens 8..15 enter as 16u
+// (nibble at bits 4..7) with their B divided by 16.  The offsets add
+// sum_t p'_t offset_t,g through one more MMA (rows = groups).
+//   acc[g]: rows = channels 16g + l/4 (+8), cols = (head l%4, hi|lo), in
+//           units of 2^(S-24);  accz: rows = groups, same cols, units 2^S.
+struct PVFrag {
+  uint32_t phi0, phi1;   // p' hi of tokens (2j, 2j+1), (2j+8, 2j+9)/16   [column head]
+  uint32_t nph0, nph1;   // -phi on lo-part lanes, 0 on hi lanes
+  uint32_t plo0, plo1;   // p' lo (/16 for the second) on lo lanes, 0 on hi lanes
+  uint32_t z0, z1;       // offset-MMA B: p' hi (hi lanes) or lo (lo lanes), unscaled
+};
+
+__device__ __forceinline__ void pv_frag(PVFrag& F, const float4 p, bool lo_lane) {
+  uint32_t h01, l01, h23, l23;
+  split_h2(p.x, p.y, h01, l01);
+  split_h2(p.z, p.w, h23, l23);
+  F.z0 = lo_lane ? l01 : h01;
+  F.z1 = lo_lane ? l23 : h23;
+  const uint32_t s16 = 0x2c002c00u;  // half2(1/16, 1/16)
+  const uint32_t h23s = h2_mul(h23, s16), l23s = h2_mul(l23, s16);
+  F.phi0 = h01;
+  F.phi1 = h23s;
+  F.nph0 = lo_lane ? (h01 ^ 0x80008000u) : 0u;
+  F.nph1 = lo_lane ? (h23s ^ 0x80008000u) : 0u;
+  F.plo0 = lo_lane ? l01 : 0u;
+  F.plo1 = lo_lane ? l23s : 0u;
+}
+
+__device__ __forceinline__ void pv_block_sub(float (&acc)[NG][4], float (&accz)[4], const PVFrag& F,
+                                            const uint8_t* rec, int lane) {
+  const uint4 w0 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + lane * 16);
+  const uint4 w1 = *reinterpret_cast<const uint4*>(rec + OFF_VCODES + 512 + lane * 16);
+  const uint32_t wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+  const uint4* sc = reinterpret_cast<const uint4*>(rec + OFF_VSCALE + (lane & 3) * 64);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 s4 = sc[q];  // groups 2q, 2q+1: (s_2j, s_2j+1), (s_2j+8, s_2j+9)
+    const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int g = 2 * q + e;
+      const uint32_t s01 = sv[2 * e], s23 = sv[2 * e + 1];
+      const uint32_t b0 = h2_fma(F.plo0, s01, h2_fma(F.phi0, s01, h2_mul(F.nph0, s01)));
+      const uint32_t b1 = h2_fma(F.plo1, s23, h2_fma(F.phi1, s23, h2_mul(F.nph1, s23)));
+      const uint32_t w = wv[(g >> 2) * 4 + (g & 3)];
+      const uint32_t w8 = w >> 8;
+      mma_f16r(acc[g], w & 0x000f000fu, w8 & 0x000f000fu, w & 0x00f000f0u, w8 & 0x00f000f0u, b0, b1);
+    }
+  }
+  const uint2 oz = *reinterpret_cast<const uint2*>(rec + OFF_VOFF + ((lane & 3) * 8 + (lane >> 2)) * 8);
+  mma_f16r(accz, oz.x, 0u, oz.y, 0u, F.z0, F.z1);
+}
+
+
 }  // namespace ckv
