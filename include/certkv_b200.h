@@ -89,6 +89,7 @@ typedef struct {
 #define CKV_ST_CAPACITY 1
 #define CKV_ST_TIER2 2
 #define CKV_ST_APPEND_BAD 3
+#define CKV_ST_APPEND_CNT 4  /* internal: CTAs of the one-token append done */
 
 typedef struct {
   double tau_cov;

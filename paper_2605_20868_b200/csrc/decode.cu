@@ -377,6 +377,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
   HeadState& hs = *reinterpret_cast<HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
   pdl_trigger();
   if (st.flow) flow_wait(st.flow + FLOW_PA_DONE * c.n_units + u, st.epoch);  // this unit's pass A
+#ifdef CKV_SELPROF
+  t_prev = gtimer();  // the profile starts once the unit's pass A is done
+#endif
 
   // the eta annotations (tail pass) and this head's pass-A split states (merge) are
   // needed later: start pulling them into L2 now

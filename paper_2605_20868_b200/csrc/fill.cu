@@ -61,10 +61,13 @@ struct FillArgs {
   int32_t n_tok;
 };
 
-__global__ void __launch_bounds__(128) k_fill(FillArgs a) {
+// Fit block j of this append for unit u (the 16 tokens at [partial | new]
+// positions 16 j ..) and write its record, Tier-2 originals and annotations at
+// block index n_blocks[u] + j -- invisible to readers until n_blocks moves.
+// v_max is raised here unless the caller commits it later (vmax_now = false).
+__device__ __forceinline__ void fill_block(const FillArgs& a, int u, int j, bool vmax_now) {
   const ckv_cache& c = a.c;
-  const int u = blockIdx.y, j = blockIdx.x, tid = threadIdx.x;
-  if (c.status[CKV_ST_APPEND_BAD]) return;  // the whole append is rejected
+  const int tid = threadIdx.x;
   const int p = c.partial_len[u];
   const int nf = (p + a.n_tok) / B;
   if (j >= nf) return;
@@ -195,13 +198,69 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
       c.nu[ib] = __double2float_ru(n);
       c.kscale_max[ib] = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
       c.tier2_valid[ib] = 1;
-      atomicMax(reinterpret_cast<int*>(&c.v_max[u]), __float_as_int(__double2float_ru(n)));
+      if (vmax_now) atomicMax(reinterpret_cast<int*>(&c.v_max[u]), __float_as_int(__double2float_ru(n)));
     }
   }
   // ---- write the record -------------------------------------------------------
   uint4* dst = reinterpret_cast<uint4*>(c.tier1 + ((size_t)u * c.max_blocks + b) * REC);
   const uint4* srcv = reinterpret_cast<const uint4*>(rec);
   for (int i = tid; i < REC / 16; i += 128) dst[i] = srcv[i];
+}
+
+__global__ void __launch_bounds__(128) k_fill(FillArgs a) {
+  if (a.c.status[CKV_ST_APPEND_BAD]) return;  // the whole append is rejected
+  fill_block(a, blockIdx.y, blockIdx.x, true);
+}
+
+// One-token append (the decode step's) in one launch: every unit checks its token,
+// writes it into its partial block -- or, when that completes the block, fits the
+// block -- at positions nobody reads yet; the last CTA commits every unit's
+// lengths and v_max, or, if any token was non-finite, counts the rejection and
+// commits nothing (same effect as k_check_finite + k_fill + k_tail).
+__global__ void __launch_bounds__(128) k_append1(FillArgs a) {
+  const ckv_cache& c = a.c;
+  const int u = blockIdx.x, tid = threadIdx.x;
+  const uint16_t kb = a.k_new[(size_t)u * D + tid], vb = a.v_new[(size_t)u * D + tid];
+  const bool bad = ((kb & 0x7c00u) == 0x7c00u) | ((vb & 0x7c00u) == 0x7c00u);
+  if (__syncthreads_or(bad) && tid == 0) atomicOr(&c.status[CKV_ST_APPEND_BAD], 1);
+  const int p = c.partial_len[u];
+  if (p + 1 < B) {
+    c.partial_k[((size_t)u * B + p) * D + tid] = kb;
+    c.partial_v[((size_t)u * B + p) * D + tid] = vb;
+  } else {
+    fill_block(a, u, 0, false);
+  }
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    last = atomicAdd(&c.status[CKV_ST_APPEND_CNT], 1) == (int)gridDim.x - 1;
+    __threadfence();
+  }
+  __syncthreads();
+  if (!last) return;
+  const bool rejected = __ldcg(&c.status[CKV_ST_APPEND_BAD]) != 0;
+  if (!rejected) {
+    for (int v = tid; v < c.n_units; v += blockDim.x) {
+      const int pv = __ldcg(&c.partial_len[v]);
+      if (pv + 1 < B) {
+        c.partial_len[v] = pv + 1;
+      } else {
+        const int nb = __ldcg(&c.n_blocks[v]);
+        if (nb < c.max_blocks) {
+          c.v_max[v] = fmaxf(__ldcg(&c.v_max[v]), __ldcg(&c.nu[(size_t)v * c.max_blocks + nb]));
+          c.n_blocks[v] = nb + 1;
+        }
+        c.partial_len[v] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (rejected) c.status[CKV_ST_NONFINITE] += 1;
+    c.status[CKV_ST_APPEND_BAD] = 0;
+    c.status[CKV_ST_APPEND_CNT] = 0;
+  }
 }
 
 __global__ void k_tail(FillArgs a) {
@@ -286,6 +345,12 @@ thread_local int g_launches = 0;
 cudaError_t launch_append(const ckv_cache* c, const uint16_t* k_new, const uint16_t* v_new,
                           int32_t n_tok, cudaStream_t s) {
   g_launches = 0;
+  if (n_tok == 1) {  // the decode step's append: one launch
+    FillArgs a{*c, k_new, v_new, 1};
+    k_append1<<<c->n_units, 128, 0, s>>>(a);
+    ++g_launches;
+    return cudaGetLastError();
+  }
   size_t n16 = (size_t)c->n_units * n_tok * D / 8;
   int grid = (int)((n16 + 255) / 256);
   if (grid > 4 * 148 * 8) grid = 4 * 148 * 8;

@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2605_20868_b200 import build, _lib
 out = os.path.join(ROOT, "paper_2605_20868_b200", "libcertkv_b200_prof.so")
-cmd = ["nvcc", *build.NVCC_FLAGS, "-DCKV_SELPROF", "-I", os.path.join(ROOT, "include"), *build.sources(), "-o", out]
+cmd = ["nvcc", *build.NVCC_FLAGS, "-shared", "-DCKV_SELPROF", "-I", os.path.join(ROOT, "include"), *build.sources(), "-o", out]
 subprocess.run(cmd, check=True)
 _lib.LIB_PATH = out
 import paper_2605_20868_b200 as ck
