@@ -14,6 +14,8 @@ const Knobs& knobs() {
     r.chunks = ch ? atoi(ch) : 1;
     r.sel_kpt = r.sel_nt = 0;
     if (const char* sv = getenv("CKV_SEL")) sscanf(sv, "%d:%d", &r.sel_kpt, &r.sel_nt);
+    const char* pc = getenv("CKV_PB_CHUNKS");
+    r.pb_chunks = pc ? atoi(pc) : 0;
     return r;
   }();
   return k;

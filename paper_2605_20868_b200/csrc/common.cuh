@@ -91,6 +91,7 @@ struct Knobs {
   bool separate_pagein;  // CKV_SEPARATE_PAGEIN: gather kernel on a side stream before pass B
   int chunks;            // CKV_CHUNKS: unit-chunked overlap of the tail with pass A
   int sel_kpt, sel_nt;   // CKV_SEL=kpt:nt forces a k_select variant (A/B runs)
+  int pb_chunks;         // CKV_PB_CHUNKS forces the pass-B chunks per unit (A/B runs)
 };
 const Knobs& knobs();
 struct DevState {

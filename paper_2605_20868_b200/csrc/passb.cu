@@ -66,7 +66,11 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
   const int nh = st.n_heads;
   const int nwork = st.n_work[u];
   float* cs = st.chunk_state + ((size_t)u * C + ck) * H * CKV_CHUNK_FLOATS;
-  if (ck * IPC >= nwork) {
+  // balanced partition (a.nchunk CTAs per unit, one chunk each) or IPC-sized chunks
+  const bool bal = a.nchunk > 0;
+  const int lo = bal ? (int)((long long)ck * nwork / a.nchunk) : ck * IPC;
+  const int hi = bal ? (int)((long long)(ck + 1) * nwork / a.nchunk) : min(nwork, lo + IPC);
+  if (lo >= hi) {
     if (tid < H) cs[tid * CKV_CHUNK_FLOATS] = ninf();
     return;
   }
@@ -109,6 +113,10 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
 
   // this warp's item sequence: chunks ck, ck+C, ...; items base+warp, +4, ...
   auto item_at = [&](int k) -> int {  // k-th item of this warp, or -1
+    if (bal) {
+      const int idx = lo + warp + k * PB_WARPS;
+      return (idx < hi) ? idx : -1;
+    }
     const int per_chunk = (IPC + PB_WARPS - 1 - warp) / PB_WARPS;
     const int chunk = k / per_chunk, within = k % per_chunk;
     const int idx = (ck + chunk * C) * IPC + warp + within * PB_WARPS;
@@ -353,7 +361,10 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     }
     __syncwarp();
     cur = nxt;
-    {  // item k + 2
+    if (bal) {  // item k + 2
+      const int idx = lo + warp + (k + 2) * PB_WARPS;
+      i1 = (idx < hi) ? idx : -1;
+    } else {
       const int idx = (ck + nx_chunk * C) * IPC + warp + nx_within * PB_WARPS;
       const int cend = min(nwork, (ck + nx_chunk * C) * IPC + IPC);
       i1 = (idx < cend) ? idx : -1;
@@ -566,7 +577,8 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   const int nh = st.n_heads;
   const size_t hu = (size_t)u * nh + h;
   const HeadState& hs = *reinterpret_cast<const HeadState*>(st.head_state + hu * CKV_HEAD_FLOATS);
-  const int C = st.n_chunks;
+  const int C = st.n_chunks;                          // chunk-state stride
+  const int Cu = a.nchunk > 0 ? a.nchunk : C;         // chunks written this step
   const int pl = c.partial_len[u];
   __shared__ int bad;
   if (tid == 0) bad = 0;
@@ -578,7 +590,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   __shared__ float red[8];
   // chunk frames: headers in parallel, one max, then independent loads per channel
   float ml = ninf();
-  for (int k = tid; k < C; k += blockDim.x) {
+  for (int k = tid; k < Cu; k += blockDim.x) {
     cm[k] = chunk(k)[0];
     ml = fmaxf(ml, cm[k]);
   }
@@ -588,7 +600,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   float M = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
   if (hs.lA > 0.f) M = fmaxf(M, hs.mA);
   if (pl > 0) M = fmaxf(M, hs.mp);
-  for (int k = tid; k < C; k += blockDim.x) csc[k] = (cm[k] == ninf()) ? 0.f : expf(cm[k] - M);
+  for (int k = tid; k < Cu; k += blockDim.x) csc[k] = (cm[k] == ninf()) ? 0.f : expf(cm[k] - M);
   __syncthreads();
   float den = 0.f, num = 0.f;
   if (hs.lA > 0.f) {
@@ -599,7 +611,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   float canary = 0.f;
   double eF = 0.0, sF = 0.0;
 #pragma unroll 8
-  for (int k = 0; k < C; ++k) {
+  for (int k = 0; k < Cu; ++k) {
     const float* cs = chunk(k);
     const float sc = csc[k];
     den += cs[1] * sc;
@@ -608,7 +620,7 @@ __global__ void __launch_bounds__(128) k_combine(StepArgs a) {
   {  // canary max and the F parts of E_val: chunks spread over the threads
     __shared__ float cw[4];
     __shared__ double ew[4], sw[4];
-    for (int k = tid; k < C; k += blockDim.x) {
+    for (int k = tid; k < Cu; k += blockDim.x) {
       if (cm[k] == ninf()) continue;
       const float* cs = chunk(k);
       canary = fmaxf(canary, cs[2]);
@@ -834,10 +846,34 @@ cudaError_t launch_union(const ckv_cache* c, const ckv_policy* pol, const ckv_st
   return cudaGetLastError();
 }
 
+// Pass-B chunks per unit: the union list is split evenly over them, and their
+// count makes units x chunks fill the SMs' pass-B slots (3 CTAs each) in whole
+// waves -- chunks of 64..256 items of the expected union (<= 4 K' blocks).
+static int pb_chunks(long long units, int kcap, int cap, int sms) {
+  if (knobs().pb_chunks > 0) return min(cap, knobs().pb_chunks);
+  const long long slots = (long long)sms * 3;
+  const int items = (4 * kcap * 15) / 16;
+  const int lo = max(1, (items + 255) / 256), hi = max(lo, min(cap, (items + 63) / 64));
+  int best = min(lo, cap);
+  double best_eff = -1.0;
+  for (int c = lo; c <= hi && c <= cap; ++c) {
+    const long long ctas = units * c;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = c;
+    }
+  }
+  return best;
+}
+
 cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                          const PageView& pv, int u0, int nu, bool pdl, bool finish, cudaStream_t s) {
   passb_attrs(c);
   StepArgs a{*c, *st, *pol, pv, u0, nu, 0, finish && st->flow && !st->queue ? 1 : 0};
+  a.nchunk = st->queue ? 0 : pb_chunks(st->plan_units > 0 ? st->plan_units : nu, st->kcap, st->n_chunks,
+                                       dev_state().sms);
   // the dataflow chain (st->flow): pass B right behind the selection, combine
   // right behind pass B, each waiting per unit (no persistent queue in that mode)
   const bool flow = st->flow != nullptr && !st->queue;
@@ -854,7 +890,7 @@ cudaError_t launch_passb(const ckv_cache* c, const ckv_policy* pol, const ckv_st
     if (slots_) k_pass_b<true><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
     else k_pass_b<false><<<grid, PB_WARPS * 32, sizeof(PassBSmem), s>>>(a);
   } else {
-    const dim3 g(st->n_chunks, nu);
+    const dim3 g(a.nchunk, nu);
     cudaError_t e = slots_ ? launch_k(pdl && flow, k_pass_b<true>, g, dim3(PB_WARPS * 32), sizeof(PassBSmem), s, a)
                            : launch_k(pdl && flow, k_pass_b<false>, g, dim3(PB_WARPS * 32), sizeof(PassBSmem), s, a);
     if (e != cudaSuccess) return e;

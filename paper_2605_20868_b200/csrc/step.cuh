@@ -51,6 +51,7 @@ struct StepArgs {
   int32_t nu;  // units in this launch (persistent kernels)
   int32_t nsplit;  // pass-A splits per unit of this step (<= st.n_splits, pa_splits())
   int32_t finish;  // the last combine CTA resolves the step (group flags, dense list)
+  int32_t nchunk;  // pass-B chunks per unit of this step, balanced over the union (0: IPC-sized)
 };
 
 __device__ __forceinline__ int rung4_group_of(const ckv_step& st, int u) {
