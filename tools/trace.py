@@ -11,6 +11,8 @@ ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--ctx", type=int, default=131072)
 ap.add_argument("--explore", type=float, default=0.0)
 ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--tier2", default="device")
+ap.add_argument("--scratch", type=int, default=-1)
 args = ap.parse_args()
 import __graft_entry__
 __graft_entry__.build()
@@ -18,7 +20,7 @@ import paper_2605_20868_b200 as ck
 from paper_2605_20868_b200.cache import _ptr
 U = args.layers * args.kv_heads
 dev = torch.device("cuda")
-cache = ck.DeviceKVCache(U, args.ctx + 4 * args.steps + 64)
+cache = ck.DeviceKVCache(U, args.ctx + 4 * args.steps + 64, tier2=args.tier2)
 g = torch.Generator(device=dev).manual_seed(1000)
 chunk = max(16, min(4096, (1 << 22) // U))
 for pos in range(0, args.ctx, chunk):
@@ -26,7 +28,8 @@ for pos in range(0, args.ctx, chunk):
     cache.append(torch.randn((U, n, 128), generator=g, device=dev).half(),
                  torch.randn((U, n, 128), generator=g, device=dev).half(), validate=False)
 pol = ck.PolicyConfig(exploration_rate=args.explore)
-dec = ck.CertifiedDecoder(cache, pol, n_heads=4, scratch=ck.ScratchCache(cache.max_blocks),
+dec = ck.CertifiedDecoder(cache, pol, n_heads=4,
+                          scratch=ck.ScratchCache(cache.max_blocks if args.scratch < 0 else args.scratch),
                           rung4_group=np.arange(U) % args.layers)
 if args.explore:
     dec.attach_rng(np.random.Generator(np.random.Philox(np.random.SeedSequence((0, 1)))))
