@@ -16,6 +16,8 @@ const Knobs& knobs() {
     if (const char* sv = getenv("CKV_SEL")) sscanf(sv, "%d:%d", &r.sel_kpt, &r.sel_nt);
     const char* pc = getenv("CKV_PB_CHUNKS");
     r.pb_chunks = pc ? atoi(pc) : 0;
+    const char* ds = getenv("CKV_DN_SPLITS");
+    r.dn_splits = ds ? atoi(ds) : 0;
     return r;
   }();
   return k;

@@ -92,6 +92,7 @@ struct Knobs {
   int chunks;            // CKV_CHUNKS: unit-chunked overlap of the tail with pass A
   int sel_kpt, sel_nt;   // CKV_SEL=kpt:nt forces a k_select variant (A/B runs)
   int pb_chunks;         // CKV_PB_CHUNKS forces the pass-B chunks per unit (A/B runs)
+  int dn_splits;         // CKV_DN_SPLITS forces the dense splits per unit (A/B runs)
 };
 const Knobs& knobs();
 struct DevState {

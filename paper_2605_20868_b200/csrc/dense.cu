@@ -15,7 +15,7 @@ namespace ckv {
 
 constexpr int DN_MAXSPLIT = 256;  // splits per dense unit (merge buffer)
 #ifndef DN_SPLITS
-#define DN_SPLITS 256
+#define DN_SPLITS 128
 #endif
 constexpr int DN_WARPS = 4;
 
@@ -137,7 +137,10 @@ __device__ __forceinline__ void dense_split_done(const DenseArgs& a, int item) {
   if (last) dense_merge_item(a, item);
 }
 
+constexpr int DN_STAGES = 2;
 struct DenseSmem {
+  uint8_t stg[DN_WARPS][DN_STAGES][2][B * D * 2];  // per warp: ring of (key tile, value tile)
+  uint64_t bar[DN_WARPS][DN_STAGES];
   float qh[H * D];
   float w[DN_WARPS][H][B];  // softmax weights x 2^14, tokens permuted (B-fragment order)
 };
@@ -149,7 +152,8 @@ struct DenseSmem {
 // weights as an fp16 hi/lo pair (column 2h + part), fp32 accumulation.  The
 // partial block is added in the merge from the state k_select computed.
 __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
-  __shared__ __align__(16) DenseSmem S;
+  extern __shared__ __align__(128) uint8_t dn_smem[];
+  DenseSmem& S = *reinterpret_cast<DenseSmem*>(dn_smem);
   __shared__ __align__(16) float ow[DN_WARPS][H][D];
   __shared__ float mw[DN_WARPS][H][2];
   DenseArgs a = a_in;
@@ -161,6 +165,13 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   // dense units so that a few of them still spread over every SM
   const int count = st.dense_list[0];
   if (count == 0) return;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < DN_WARPS; ++w)
+      for (int s = 0; s < DN_STAGES; ++s) mbar_init(&S.bar[w][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int kb = 0;  // blocks this warp has pushed through its ring (stage / parity across tasks)
   // ~384 tasks in all: long splits (little merge work) when many units are dense,
   // up to DN_SPLITS per unit when only a few are (latency-bound otherwise)
   a.n_dsplit = (st.dense_splits > 0) ? min(st.n_dsplit_cap, st.dense_splits)
@@ -205,20 +216,31 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   const PageView& pv = a.pv;
   const int32_t* kslot = pv.kslots ? pv.kslot_of + (size_t)u * pv.kstride : nullptr;
   const int32_t* vslot = pv.vslots ? pv.vslot_of + (size_t)u * pv.vstride : nullptr;
-  int ksl = (kslot && b0 + warp < b1) ? kslot[b0 + warp] : -1;
-  int vsl = (vslot && b0 + warp < b1) ? vslot[b0 + warp] : -1;
-  for (int b = b0 + warp; b < b1; b += DN_WARPS) {
-    const uint4* vf = reinterpret_cast<const uint4*>(
-        (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D);
-    const uint4* kf = reinterpret_cast<const uint4*>(
-        (ksl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + ksl) * B * D : c.tier2_k + (ubk + b) * B * D);
-    const int bn = b + DN_WARPS;  // the next block's slots, loaded one iteration ahead
-    ksl = (kslot && bn < b1) ? kslot[bn] : -1;
-    vsl = (vslot && bn < b1) ? vslot[bn] : -1;
+  // this warp's blocks b0 + warp + 4 i stream through a DN_STAGES ring of bulk copies
+  const int nmine = (b1 - b0 > warp) ? (b1 - b0 - warp + DN_WARPS - 1) / DN_WARPS : 0;
+  auto issue = [&](int i) {  // lane 0
+    const int b = b0 + warp + DN_WARPS * i;
+    const int s2 = (kb + i) % DN_STAGES;
+    const int ksl = kslot ? kslot[b] : -1, vsl = vslot ? vslot[b] : -1;
+    const uint16_t* ks = (ksl >= 0) ? pv.kslots + ((size_t)u * pv.kcap + ksl) * B * D : c.tier2_k + (ubk + b) * B * D;
+    const uint16_t* vs = (vsl >= 0) ? pv.vslots + ((size_t)u * pv.vcap + vsl) * B * D : c.tier2_v + (ubk + b) * B * D;
+    mbar_expect_tx(&S.bar[warp][s2], 2 * B * D * 2);
+    bulk_g2s(S.stg[warp][s2][0], ks, B * D * 2, &S.bar[warp][s2]);
+    bulk_g2s(S.stg[warp][s2][1], vs, B * D * 2, &S.bar[warp][s2]);
+  };
+  if (lane == 0)
+    for (int i = 0; i < DN_STAGES && i < nmine; ++i) issue(i);
+  for (int i = 0; i < nmine; ++i) {
+    const int s2 = (kb + i) % DN_STAGES;
+    mbar_wait(&S.bar[warp][s2], (uint32_t)((kb + i) / DN_STAGES) & 1u);
+    const uint4* kf = reinterpret_cast<const uint4*>(S.stg[warp][s2][0]);
+    const uint4* vf = reinterpret_cast<const uint4*>(S.stg[warp][s2][1]);
     uint4 av[NG];
 #pragma unroll
     for (int g = 0; g < NG; ++g) av[g] = vf[g * 32 + lane];
     const float2 s = orig_block(f16, kf, lane);
+    __syncwarp();  // every lane has read the stage: refill it
+    if (lane == 0 && i + DN_STAGES < nmine) issue(i + DN_STAGES);
     float bmx = fmaxf(s.x, s.y);
     bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 4));
     bmx = fmaxf(bmx, __shfl_xor_sync(0xffffffffu, bmx, 8));
@@ -246,6 +268,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
     for (int g = 0; g < NG; ++g) mma_f16r(acc[g], av[g].x, av[g].y, av[g].z, av[g].w, bb0, bb1);
     __syncwarp();
   }
+  kb += nmine;
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 4);
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 8);
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 16);
@@ -295,6 +318,7 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scrat
                          int host_max_tokens, bool resolved, cudaStream_t s) {
   (void)host_max_tokens;
   DenseArgs a{*c, *st, resolved ? 1 : 0, 1, 0, PageView{}};
+  if (a.st.dense_splits <= 0 && knobs().dn_splits > 0) a.st.dense_splits = knobs().dn_splits;
   if (sc && (sc->key_slots || sc->value_slots)) {
     a.pv.kslots = sc->key_capacity > 0 ? sc->key_slots : nullptr;
     a.pv.vslots = sc->value_capacity > 0 ? sc->value_slots : nullptr;
@@ -305,21 +329,22 @@ cudaError_t launch_dense(const ckv_cache* c, const ckv_step* st, const ckv_scrat
     a.pv.kslot_of = sc->key_lru + lru_slot_offset(c->max_blocks, sc->key_capacity);
     a.pv.vslot_of = sc->value_lru + lru_slot_offset(c->max_blocks, sc->value_capacity);
   }
+  set_max_dyn_smem(k_dense, (int)sizeof(DenseSmem));
   DevState& ds = dev_state();
   if (!ds.dense_slots) {
     int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dense, DN_WARPS * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dense, DN_WARPS * 32, sizeof(DenseSmem));
     ds.dense_slots = max(1, ds.sms * max(1, per));
   }
   const int slots = ds.dense_slots;
   if (resolved) {  // right behind the combine that resolved the step (PDL)
-    cudaError_t e = launch_k(true, k_dense, dim3(slots), dim3(DN_WARPS * 32), 0, s, a);
+    cudaError_t e = launch_k(true, k_dense, dim3(slots), dim3(DN_WARPS * 32), sizeof(DenseSmem), s, a);
     g_launches += 1;
     return e;
   }
   cudaMemsetAsync(st->dense_list, 0, sizeof(int32_t) * (1 + c->n_units), s);  // count + done counters
   k_resolve<<<(c->n_units + 255) / 256, 256, 0, s>>>(a);
-  k_dense<<<slots, DN_WARPS * 32, 0, s>>>(a);
+  k_dense<<<slots, DN_WARPS * 32, sizeof(DenseSmem), s>>>(a);
   g_launches += 2;
   // the dataflow path (resolved) expects the step-wide requests cleared
   cudaMemsetAsync(st->group_flags, 0, sizeof(int32_t) * st->n_groups, s);

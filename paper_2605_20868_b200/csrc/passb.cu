@@ -213,9 +213,14 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       mbar_expect_tx(&S.bar[warp][stg], REC + (keys ? B * D * 2 : 0));
       bulk_g2s(S.rec[warp][stg], t1base + (size_t)b2 * REC, REC, &S.bar[warp][stg]);
     }
-    // a value tile missed this step is read from host Tier-2 in the item's value
-    // branch: start pulling it into L2 now
-    if (SLOTS && m.vsl >= 0 && (m.vsl & 0x40000000)) prefetch_l2(c.tier2_v + (ubk + b2) * B * D, B * D * 2);
+    // the value tile of a value-promoted item is read with plain loads in its value
+    // branch (from its HBM slot, or from Tier-2 -- host RAM when missed this step):
+    // start pulling it into L2 an item ahead, off the loop's latency
+    if ((uint32_t)m.e >> 28) {
+      const bool in_slot = SLOTS && m.vsl >= 0 && !(m.vsl & 0x40000000);
+      prefetch_l2(in_slot ? pv.vslots + ((size_t)u * pv.vcap + m.vsl) * B * D : c.tier2_v + (ubk + b2) * B * D,
+                  B * D * 2);
+    }
     if (keys) {
       const uint16_t* src = (m.sl >= 0 && !(m.sl & 0x40000000))
                                 ? pv.kslots + ((size_t)u * pv.kcap + m.sl) * B * D
