@@ -333,6 +333,7 @@ struct SelSmem {
   int wsum[32];
   int wsum2[32];
   int misc[16];
+  uint32_t krange[2];
   double redd[40];
   float redf[40];
 };
@@ -395,9 +396,74 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
 #pragma unroll
   for (int j = 0; j < KPT; ++j) kk[j] = (BJ(j) < nb) ? okey(__ldcg(lm + BJ(j))) : 0u;
 
+  // ---- the pass-A split states, loaded right away (their latency overlaps the
+  // keys'): thread (g, d) merges splits g, g + SG, ... online, the SG group
+  // partials are combined after the barrier below
+  constexpr int SG = NT / D;
+  const int nsp = min(a.nsplit, nb);
+  float* mrg = reinterpret_cast<float*>(S.cand);  // [SG][D] O, then [SG] m, l, delta (free until the gather)
+  {
+    const int g = tid / D, d = tid % D;
+    const float* spb = st.split_state + (((size_t)u * st.n_splits) * H + h) * CKV_SPLIT_FLOATS;
+    float m_t = ninf(), l_t = 0.f, o_t = 0.f, d_t = 0.f;
+    constexpr int MU = KPT <= 16 ? 4 : 1;  // splits in flight per thread (register budget)
+    for (int s0 = g; s0 < nsp; s0 += SG * MU) {
+      float m[MU], l[MU], dl[MU], o[MU];
+#pragma unroll
+      for (int q = 0; q < MU; ++q) {
+        const float* sp = spb + (size_t)(s0 + q * SG) * H * CKV_SPLIT_FLOATS;
+        const bool ok = s0 + q * SG < nsp;
+        m[q] = ok ? sp[0] : ninf();
+        l[q] = ok ? sp[1] : 0.f;
+        dl[q] = ok ? sp[2] : 0.f;
+        o[q] = ok ? sp[4 + d] : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < MU; ++q) {
+        d_t = fmaxf(d_t, dl[q]);
+        if (m[q] != ninf()) {
+          const float mn = fmaxf(m_t, m[q]);
+          const float a0 = (m_t == ninf()) ? 0.f : expf(m_t - mn), a1 = expf(m[q] - mn);
+          l_t = fmaf(l_t, a0, l[q] * a1);
+          o_t = fmaf(o_t, a0, o[q] * a1);
+          m_t = mn;
+        }
+      }
+    }
+    mrg[g * D + d] = o_t;
+    if (d == 0) {
+      mrg[SG * D + g] = m_t;
+      mrg[SG * D + SG + g] = l_t;
+      mrg[SG * D + 2 * SG + g] = d_t;
+    }
+  }
   if (tid < D) S.qv[tid] = (float)(st.q[hu * D + tid] * 0.08838834764831845);
   for (int i = tid; i < (c.max_blocks + 31) / 32; i += NT) fmask[i] = 0u;
   __syncthreads();
+  if (tid < D) {  // combine the SG group partials of the pass-A splits
+    float M = ninf(), dm = 0.f;
+#pragma unroll
+    for (int g = 0; g < SG; ++g) {
+      M = fmaxf(M, mrg[SG * D + g]);
+      dm = fmaxf(dm, mrg[SG * D + 2 * SG + g]);
+    }
+    float L = 0.f, O = 0.f;
+    if (M != ninf()) {
+#pragma unroll
+      for (int g = 0; g < SG; ++g) {
+        const float mg = mrg[SG * D + g];
+        const float sc = (mg == ninf()) ? 0.f : expf(mg - M);
+        L = fmaf(mrg[SG * D + SG + g], sc, L);
+        O = fmaf(mrg[g * D + tid], sc, O);
+      }
+    }
+    hs.oA[tid] = O;
+    if (tid == 0) {
+      hs.mA = M;
+      hs.lA = L;
+      hs.delta = dm;
+    }
+  }
 
   SELPROF(1);
   // ---- partial block on originals (attention.py:98-104) ------------------------
@@ -424,50 +490,42 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
   }
 
   SELPROF(2);
-  // ---- merge the pass-A splits: headers in parallel, then independent loads ---------
-  const int nsp = min(a.nsplit, nb);
-  {
-    const float* spb = st.split_state + (((size_t)u * st.n_splits) * H + h) * CKV_SPLIT_FLOATS;
-    float mloc = ninf(), dloc = 0.f;
-    for (int s2 = tid; s2 < nsp; s2 += NT) {
-      const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
-      mloc = fmaxf(mloc, sp[0]);
-      dloc = fmaxf(dloc, sp[2]);
-    }
-    const float2 Mdm = block_max_f2(mloc, dloc, reinterpret_cast<float*>(S.cum));  // S.cum is written below
-    const float M = Mdm.x, dm = Mdm.y;
-    for (int s2 = tid; s2 < nsp; s2 += NT) {
-      const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
-      S.cum[s2] = (sp[0] == ninf()) ? 0.0 : (double)expf(sp[0] - M);
-    }
-    __syncthreads();
-    float L = 0.f, O = 0.f;
-    if (M != ninf() && tid < D) {
-#pragma unroll 16
-      for (int s2 = 0; s2 < nsp; ++s2) {
-        const float* sp = spb + (size_t)s2 * H * CKV_SPLIT_FLOATS;
-        const float sc = (float)S.cum[s2];
-        L += sp[1] * sc;
-        O += sp[4 + tid] * sc;
-      }
-    }
-    if (tid < D) hs.oA[tid] = O;
-    if (tid == 0) {
-      hs.mA = M;
-      hs.lA = L;
-      hs.delta = dm;
-      hs.mp = mp;
-      hs.lp = lp;
-    }
-    __syncthreads();
+  if (tid == 0) {
+    hs.mp = mp;
+    hs.lp = lp;
   }
-
   SELPROF(3);
   // ---- lse over l'_b and the partial (attention.py:170-179) ------------------------
+  // (with the key range the radix select starts from: one barrier round)
   float lmax = lmp;
+  uint32_t kmn_r = 0xffffffffu, kmx_r = 0u;
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) lmax = fmaxf(lmax, (BJ(j) < nb) ? ukey(kk[j]) : ninf());
-  lmax = block_max_f(lmax, S.redf);
+  for (int j = 0; j < KPT; ++j) {
+    if (BJ(j) < nb) {
+      lmax = fmaxf(lmax, ukey(kk[j]));
+      kmn_r = min(kmn_r, kk[j]);
+      kmx_r = max(kmx_r, kk[j]);
+    }
+  }
+  lmax = warp_max(lmax);
+  kmn_r = __reduce_min_sync(0xffffffffu, kmn_r);
+  kmx_r = __reduce_max_sync(0xffffffffu, kmx_r);
+  if (lane == 0) {
+    S.redf[warp] = lmax;
+    S.wsum[warp] = (int)kmn_r;
+    S.wsum2[warp] = (int)kmx_r;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < NT / 32; ++w) {
+    lmax = fmaxf(lmax, S.redf[w]);
+    kmn_r = min(kmn_r, (uint32_t)S.wsum[w]);
+    kmx_r = max(kmx_r, (uint32_t)S.wsum2[w]);
+  }
+  if (tid == 0) {  // read again by the radix select (behind block_sum_d's barriers)
+    S.krange[0] = kmn_r;
+    S.krange[1] = kmx_r;
+  }
   float sef = 0.f;
   const float lmax2 = lmax * 1.4426950408889634f;
 #pragma unroll
@@ -501,27 +559,9 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
   if (ksel > 0) {
     // digits of (key - min key), 11 bits at a time from the top of the occupied
     // range, so the first histogram spreads over the keys actually present
-    uint32_t kmn = 0xffffffffu, kmx = 0u;
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      if (BJ(j) < nb) {
-        kmn = min(kmn, skey(j));
-        kmx = max(kmx, skey(j));
-      }
-    }
-    kmn = __reduce_min_sync(0xffffffffu, kmn);
-    kmx = __reduce_max_sync(0xffffffffu, kmx);
-    if (lane == 0) {
-      S.wsum[warp] = (int)kmn;
-      S.wsum2[warp] = (int)kmx;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < NT / 32; ++w) {
-      kmn = min(kmn, (uint32_t)S.wsum[w]);
-      kmx = max(kmx, (uint32_t)S.wsum2[w]);
-    }
-    __syncthreads();
+    // skey is monotone in the key: the range of skey is skey of the key range
+    const uint32_t kmn = S.krange[0] < zk ? zk - 1u : S.krange[0];
+    const uint32_t kmx = S.krange[1] < zk ? zk - 1u : S.krange[1];
     const int nbits = (kmx > kmn) ? 32 - __clz(kmx - kmn) : 0;
     // Radix passes until the keys >= the current bin's lower edge number at
     // most SEL_MAXSORT (normally one pass): those are the candidates, sorted
