@@ -67,7 +67,7 @@ __global__ void k_resolve(DenseArgs a) {
 
 // Merge the splits of one dense item and overwrite the output of its dense
 // heads (run by the last split CTA of the item to finish).
-__device__ void dense_merge_item(const DenseArgs& a, int item) {
+__device__ void dense_merge_item(const DenseArgs& a, int item, float* scratch) {
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   const int e = st.dense_list[1 + c.n_units + item];
@@ -76,7 +76,9 @@ __device__ void dense_merge_item(const DenseArgs& a, int item) {
   const int tid = threadIdx.x;
   const int pl = c.partial_len[u];
   const int ns = a.n_dsplit;
-  __shared__ float sm_m[H][DN_MAXSPLIT], sm_sc[H][DN_MAXSPLIT];
+  // (scratch: the CTA's K/V stage buffers, free once its blocks are consumed)
+  float (*sm_m)[DN_MAXSPLIT] = reinterpret_cast<float (*)[DN_MAXSPLIT]>(scratch);
+  float (*sm_sc)[DN_MAXSPLIT] = reinterpret_cast<float (*)[DN_MAXSPLIT]>(scratch + H * DN_MAXSPLIT);
   __shared__ float red[H][4];
   const float* p0 = st.dense_part + ((size_t)item * st.n_dsplit_cap * H) * 132;
   // per-split maxima -> per-head frame, splits spread over the threads
@@ -122,7 +124,7 @@ __device__ void dense_merge_item(const DenseArgs& a, int item) {
 
 // Called by every split CTA of a dense item once its state is written: the
 // last one merges (device-scope counter, reset for the next step).
-__device__ __forceinline__ void dense_split_done(const DenseArgs& a, int item) {
+__device__ __forceinline__ void dense_split_done(const DenseArgs& a, int item, float* scratch) {
   __shared__ int last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -134,7 +136,7 @@ __device__ __forceinline__ void dense_split_done(const DenseArgs& a, int item) {
     __threadfence();
   }
   __syncthreads();
-  if (last) dense_merge_item(a, item);
+  if (last) dense_merge_item(a, item, scratch);
 }
 
 constexpr int DN_STAGES = 2;
@@ -154,8 +156,11 @@ struct DenseSmem {
 __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   extern __shared__ __align__(128) uint8_t dn_smem[];
   DenseSmem& S = *reinterpret_cast<DenseSmem*>(dn_smem);
-  __shared__ __align__(16) float ow[DN_WARPS][H][D];
-  __shared__ float mw[DN_WARPS][H][2];
+  // a warp's split partials (O, then m / l) go to its own stage buffers once it
+  // has consumed its blocks; the merge scratch is the whole stage area
+  auto ow = [&](int w) { return reinterpret_cast<float (*)[D]>(S.stg[w][0][0]); };
+  auto mw = [&](int w) { return reinterpret_cast<float (*)[2]>(S.stg[w][0][0] + H * D * 4); };
+  float* mscratch = reinterpret_cast<float*>(S.stg);
   DenseArgs a = a_in;
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
@@ -174,8 +179,22 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   int kb = 0;  // blocks this warp has pushed through its ring (stage / parity across tasks)
   // ~384 tasks in all: long splits (little merge work) when many units are dense,
   // up to DN_SPLITS per unit when only a few are (latency-bound otherwise)
-  a.n_dsplit = (st.dense_splits > 0) ? min(st.n_dsplit_cap, st.dense_splits)
-                                       : min(st.n_dsplit_cap, min(DN_SPLITS, max(32, (384 + count - 1) / count)));
+  if (st.dense_splits > 0) {
+    a.n_dsplit = min(st.n_dsplit_cap, st.dense_splits);
+  } else if (count <= (int)gridDim.x) {  // one wave of tasks
+    a.n_dsplit = min(st.n_dsplit_cap, min(DN_SPLITS, (int)gridDim.x / count));
+  } else {  // the split count with the fewest waves per unit of work (ties -> fewer splits)
+    int best = 1;
+    long long bw = (count + gridDim.x - 1) / gridDim.x;  // waves x best, compared as fractions
+    for (int n = 2; n <= 16 && n <= st.n_dsplit_cap; ++n) {
+      const long long w = ((long long)count * n + gridDim.x - 1) / gridDim.x;
+      if (w * best < bw * n) {
+        best = n;
+        bw = w;
+      }
+    }
+    a.n_dsplit = best;
+  }
   for (int task = blockIdx.x; task < count * a.n_dsplit; task += gridDim.x) {
   const int item = task / a.n_dsplit, sp = task % a.n_dsplit;
   const int e = st.dense_list[1 + c.n_units + item];
@@ -186,10 +205,11 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   const int bps = max(1, (nb + a.n_dsplit - 1) / a.n_dsplit);
   const int b0 = sp * bps, b1 = min(nb, b0 + bps);
   float* outp = st.dense_part + (((size_t)item * st.n_dsplit_cap + sp) * H) * 132;
-  __syncthreads();  // the previous task is done with S / ow / mw
+  fence_proxy_async();  // this thread's generic smem writes before the next bulk copies
+  __syncthreads();  // the previous task is done with S (stages, partials, merge)
   if (b0 >= b1) {
     for (int i = tid; i < H * 132; i += blockDim.x) outp[i] = (i % 132 == 0) ? dninf() : 0.f;
-    dense_split_done(a, item);
+    dense_split_done(a, item, mscratch);
     continue;
   }
   for (int i = tid; i < H * D; i += blockDim.x) {
@@ -273,25 +293,25 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 8);
   l_h += __shfl_xor_sync(0xffffffffu, l_h, 16);
   if (lane < H) {
-    mw[warp][lane][0] = m_h;
-    mw[warp][lane][1] = l_h;
+    mw(warp)[lane][0] = m_h;
+    mw(warp)[lane][1] = l_h;
   }
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
-    ow[warp][h][16 * g + t0] = (acc[g][0] + acc[g][1]) * (1.f / 16384.f);
-    ow[warp][h][16 * g + t0 + 8] = (acc[g][2] + acc[g][3]) * (1.f / 16384.f);
+    ow(warp)[h][16 * g + t0] = (acc[g][0] + acc[g][1]) * (1.f / 16384.f);
+    ow(warp)[h][16 * g + t0 + 8] = (acc[g][2] + acc[g][3]) * (1.f / 16384.f);
   }
   __syncthreads();
   for (int hh = 0; hh < H; ++hh) {
     float M = dninf();
-    for (int w = 0; w < DN_WARPS; ++w) M = fmaxf(M, mw[w][hh][0]);
+    for (int w = 0; w < DN_WARPS; ++w) M = fmaxf(M, mw(w)[hh][0]);
     float L = 0.f, O = 0.f;
     if (M != dninf()) {
       for (int w = 0; w < DN_WARPS; ++w) {
-        if (mw[w][hh][0] == dninf()) continue;
-        const float sc = expf(mw[w][hh][0] - M);
-        L += mw[w][hh][1] * sc;
-        O += ow[w][hh][tid] * sc;
+        if (mw(w)[hh][0] == dninf()) continue;
+        const float sc = expf(mw(w)[hh][0] - M);
+        L += mw(w)[hh][1] * sc;
+        O += ow(w)[hh][tid] * sc;
       }
     }
     if (tid == 0) {
@@ -300,7 +320,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
     }
     outp[hh * 132 + 4 + tid] = O;
   }
-  dense_split_done(a, item);
+  dense_split_done(a, item, mscratch);
   }  // task loop
 }
 
