@@ -280,15 +280,16 @@ __device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
   return r;
 }
 
-// Block reductions: every thread folds the per-warp partials itself, in warp order
-// (so all threads hold the same bits), two barriers per call.
+// Block reductions: every warp folds the per-warp partials itself, lane w taking
+// warp w's, with the same xor butterfly (addition is commutative, so all threads
+// hold the same bits), two barriers per call.
 __device__ __forceinline__ double block_sum_d(double v, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   v = warp_sum_d(v);
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  double t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+  t = warp_sum_d(t);
   __syncthreads();
   return t;
 }
@@ -298,8 +299,8 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
   v = warp_max(v);
   if (lane == 0) red[warp] = v;
   __syncthreads();
-  float t = red[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, red[w]);
+  float t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : ninf();
+  t = warp_max(t);
   __syncthreads();
   return t;
 }
@@ -314,11 +315,8 @@ __device__ __forceinline__ float2 block_max_f2(float a, float b, float* red) {
     red[32 + warp] = b;
   }
   __syncthreads();
-  float ta = red[0], tb = red[32];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-    ta = fmaxf(ta, red[w]);
-    tb = fmaxf(tb, red[32 + w]);
-  }
+  const bool in = lane < (int)(blockDim.x >> 5);
+  const float ta = warp_max(in ? red[lane] : ninf()), tb = warp_max(in ? red[32 + lane] : ninf());
   __syncthreads();
   return make_float2(ta, tb);
 }
@@ -516,11 +514,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
     S.wsum2[warp] = (int)kmx_r;
   }
   __syncthreads();
-#pragma unroll
-  for (int w = 0; w < NT / 32; ++w) {
-    lmax = fmaxf(lmax, S.redf[w]);
-    kmn_r = min(kmn_r, (uint32_t)S.wsum[w]);
-    kmx_r = max(kmx_r, (uint32_t)S.wsum2[w]);
+  {
+    const bool in = lane < NT / 32;
+    lmax = warp_max(in ? S.redf[lane] : ninf());
+    kmn_r = __reduce_min_sync(0xffffffffu, in ? (uint32_t)S.wsum[lane] : 0xffffffffu);
+    kmx_r = __reduce_max_sync(0xffffffffu, in ? (uint32_t)S.wsum2[lane] : 0u);
   }
   if (tid == 0) {  // read again by the radix select (behind block_sum_d's barriers)
     S.krange[0] = kmn_r;
@@ -664,10 +662,12 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
     // rank sort (composite keys are distinct): position = #greater; the
     // candidate list is read as broadcast 16-byte pairs (a thread per candidate
     // measured faster than warp-cooperative variants)
+    // (a thread per candidate, the list read as broadcast 16-byte pairs: measured
+    // faster than splitting a candidate's count over several lanes)
+    const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(S.cand);
     for (int i = tid; i < n_sorted; i += NT) {
       const unsigned long long x = S.cand[i];
       int r = 0;
-      const ulonglong2* c2 = reinterpret_cast<const ulonglong2*>(S.cand);
       int j = 0;
 #pragma unroll 4
       for (; j + 1 < n_sorted; j += 2) {
@@ -686,21 +686,30 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
     S.cum[i] = (double)expf(ukey((uint32_t)(S.sortk[i] >> 32)) - lsef);
   }
   __syncthreads();
-  if (warp == 0) {  // prefix sum in fp64 along the mass order (one warp, chunked)
-    double carry = pmass;
-    for (int b0 = 0; b0 < n_sorted; b0 += 32) {
-      const int i = b0 + lane;
-      double x = (i < n_sorted) ? S.cum[i] : 0.0;
+  // prefix sum in fp64 along the mass order: 32-entry chunks scanned by the warps
+  // in parallel, then each chunk adds the carry pmass + T_0 + ... + T_{c-1} summed
+  // in chunk order (the same operations as one warp walking the chunks)
+  const int nchk = (n_sorted + 31) / 32;
+  double* ctot = S.redd;  // chunk totals (<= 32)
+  for (int ch = warp; ch < nchk; ch += NT / 32) {
+    const int i = ch * 32 + lane;
+    double x = (i < n_sorted) ? S.cum[i] : 0.0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        double y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      if (i < n_sorted) S.cum[i] = carry + x;
-      carry += __shfl_sync(0xffffffffu, x, 31);
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
+    if (i < n_sorted) S.cum[i] = x;
+    if (lane == 31) ctot[ch] = x;
   }
   if (tid == 0) S.misc[4] = -1;
+  __syncthreads();
+  for (int ch = warp; ch < nchk; ch += NT / 32) {
+    double carry = pmass;
+    for (int c2 = 0; c2 < ch; ++c2) carry += ctot[c2];
+    const int i = ch * 32 + lane;
+    if (i < n_sorted) S.cum[i] = carry + S.cum[i];
+  }
   __syncthreads();
   for (int i = tid; i < n_sorted; i += NT)
     if (S.cum[i] >= pol.tau_cov && (i == 0 || S.cum[i - 1] < pol.tau_cov)) S.misc[4] = i + 1;
@@ -855,18 +864,17 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
     }
     if (lane == 31) S.wsum[warp] = x;
     __syncthreads();
-    float tm = S.redf[0];
-    double ta = 0.0, te = 0.0;
-    int before = 0, tot = 0;
-#pragma unroll 8
-    for (int w = 0; w < NT / 32; ++w) {
-      tm = fmaxf(tm, S.redf[w]);
-      ta += S.redd[w];
-      te += S.cum[w];
-      const int ws = S.wsum[w];
-      before += (w < warp) ? ws : 0;
-      tot += ws;
+    const bool in = lane < NT / 32;
+    const float tm = warp_max(in ? S.redf[lane] : ninf());
+    const double ta = warp_sum_d(in ? S.redd[lane] : 0.0), te = warp_sum_d(in ? S.cum[lane] : 0.0);
+    int sc = in ? S.wsum[lane] : 0;  // inclusive scan of the warp counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, sc, o);
+      if (lane >= o) sc += y;
     }
+    const int tot = __shfl_sync(0xffffffffu, sc, 31);
+    const int before = (warp > 0) ? __shfl_sync(0xffffffffu, sc, warp - 1) : 0;
     __syncthreads();
     tmx = tm;
     at = ta;
