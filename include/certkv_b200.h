@@ -203,6 +203,14 @@ typedef struct {
   unsigned long long* trace; /* [32][2] optional timeline (profiling): per kernel of the step,
                                the first CTA start / last CTA end (globaltimer ns) by
                                atomicMin / atomicMax; the caller resets it (NULL: off) */
+  void* host_report;        /* optional pinned host buffer the device can write (e.g.
+                               cudaHostAlloc / pinned torch memory under unified addressing):
+                               the step's last kernel writes the step's bound report there,
+                               cert[n_units][n_heads] | the cache's 8 status words |
+                               page_stats[n_units][4] (when set) | explore_n[n_units][n_heads]
+                               (when set), each part 16-byte aligned
+                               (ckv_report_bytes), so the caller reads it after the step's
+                               completion with no device-to-host copies (NULL: off) */
 } ckv_step;
 
 /* trace slots */
@@ -251,6 +259,9 @@ int32_t ckv_version(void);
  * ckv_policy, ckv_cert, ckv_step, ckv_scratch (lets a binding check its mirrors) */
 void ckv_struct_sizes(int32_t* out);
 int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity);
+/* Byte size and part offsets of the host_report layout: out[0..3] = total bytes,
+ * offset of the status words, of page_stats, of explore_n (cert at 0). */
+void ckv_report_layout(int32_t n_units, int32_t n_heads, int64_t* out);
 /* Initialise both LRU states and zero the cumulative counters. */
 ckv_status ckv_scratch_init(int32_t n_units, int32_t max_blocks, const ckv_scratch* s, void* stream);
 

@@ -67,7 +67,7 @@ class CkvStep(ctypes.Structure):
                 ("queue", P), ("stash", P), ("stash_epoch", P), ("epoch", I32),
                 ("stash_margin", ctypes.c_float), ("plan_units", I32), ("dense_splits", I32),
                 ("explore_rng", P), ("explore_rate", ctypes.c_double), ("explore_work", P),
-                ("flow", P), ("trace", P)]
+                ("flow", P), ("trace", P), ("host_report", P)]
 
 
 class CkvScratch(ctypes.Structure):
@@ -95,6 +95,7 @@ def load():
         "ckv_version": (I32, []),
         "ckv_struct_sizes": (None, [P]),
         "ckv_lru_words": (I32, [I32, I32]),
+        "ckv_report_layout": (None, [I32, I32, P]),
         "ckv_scratch_init": (I32, [I32, I32, ctypes.POINTER(CkvScratch), P]),
         "ckv_plan": (I32, [I32, I32, I32, ctypes.POINTER(CkvPolicy), ctypes.POINTER(CkvStep)]),
         "ckv_append": (I32, [ctypes.POINTER(CkvCache), P, P, I32, P]),
@@ -132,7 +133,7 @@ def exported_symbols():
             "ckv_reset", "ckv_decode_step", "ckv_read_tier1", "ckv_fault_offset",
             "ckv_tier2_drop", "ckv_block_logmass", "ckv_fused_attend", "ckv_last_launches",
             "ckv_f64_to_f16", "ckv_last_error", "ckv_decode_begin", "ckv_decode_end",
-            "ckv_decode_flags", "ckv_decode_finish", "ckv_struct_sizes"]
+            "ckv_decode_flags", "ckv_decode_finish", "ckv_struct_sizes", "ckv_report_layout"]
 
 
 def check(code, what):

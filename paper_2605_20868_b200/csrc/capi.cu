@@ -74,6 +74,7 @@ cudaError_t launch_decode(const ckv_cache*, const ckv_policy*, const ckv_step*, 
 cudaError_t launch_dense(const ckv_cache*, const ckv_step*, const ckv_scratch*, int, bool, cudaStream_t);
 bool decode_flow(const ckv_cache*, const ckv_step*);
 cudaError_t launch_group_flags(const ckv_cache*, const ckv_step*, cudaStream_t);
+cudaError_t launch_publish(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_explore(const ckv_cache*, const ckv_policy*, const ckv_step*, int, cudaStream_t);
 cudaError_t launch_explore_draw(const ckv_cache*, const ckv_step*, cudaStream_t);
 cudaError_t launch_scratch(const ckv_cache*, const ckv_step*, const ckv_scratch*, cudaStream_t);
@@ -109,6 +110,11 @@ void ckv_struct_sizes(int32_t* out) {
   out[2] = (int32_t)sizeof(ckv_cert);
   out[3] = (int32_t)sizeof(ckv_step);
   out[4] = (int32_t)sizeof(ckv_scratch);
+}
+
+void ckv_report_layout(int32_t n_units, int32_t n_heads, int64_t* out) {
+  if (!out) return;
+  ckv::report_layout(n_units, n_heads, out);
 }
 
 int32_t ckv_lru_words(int32_t max_blocks, int32_t capacity) {
@@ -223,7 +229,9 @@ ckv_status ckv_decode_finish(const ckv_cache* c, ckv_step* st, const ckv_scratch
   ckv_policy dummy{};
   dummy.k_max = 1;
   if (!step_ok(c, &dummy, st, host_max_blocks)) return CKV_EINVAL;
-  return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, false, S(stream)));
+  cudaError_t e = ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, false, S(stream));
+  if (e == cudaSuccess && st->host_report) e = ckv::launch_publish(c, st, S(stream));
+  return st_of(e);
 }
 
 ckv_status ckv_decode_end(const ckv_cache* c, const ckv_policy* pol, ckv_step* st,
@@ -240,7 +248,9 @@ ckv_status ckv_decode_step(const ckv_cache* c, const ckv_policy* pol, ckv_step* 
     // Rung 4 and the dense list, the dense pass launches right behind it
     ckv_status r = decode_begin(c, pol, st, scratch, host_max_blocks, true, stream);
     if (r != CKV_OK) return r;
-    return st_of(ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, true, S(stream)));
+    cudaError_t e = ckv::launch_dense(c, st, scratch, (host_max_blocks + 1) * CKV_BLOCK, true, S(stream));
+    if (e == cudaSuccess && st->host_report) e = ckv::launch_publish(c, st, S(stream));
+    return st_of(e);
   }
   ckv_status r = ckv_decode_begin(c, pol, st, scratch, host_max_blocks, stream);
   if (r != CKV_OK) return r;

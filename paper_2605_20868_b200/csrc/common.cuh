@@ -95,6 +95,16 @@ struct Knobs {
   int dn_splits;         // CKV_DN_SPLITS forces the dense splits per unit (A/B runs)
 };
 const Knobs& knobs();
+// host_report layout (ckv_report_layout): cert | status[8] | page_stats | explore_n
+inline void report_layout(int n_units, int n_heads, int64_t* out) {
+  auto up = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
+  const int64_t cert = up((int64_t)n_units * n_heads * (int64_t)sizeof(ckv_cert));
+  const int64_t status = cert, ps = up(status + 8 * 4), en = up(ps + (int64_t)n_units * 16);
+  out[0] = up(en + (int64_t)n_units * n_heads * 4);
+  out[1] = status;
+  out[2] = ps;
+  out[3] = en;
+}
 struct DevState {
   int sms = 0;
   int dense_slots = 0;

@@ -325,6 +325,62 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
 }
 
 
+// The step's bound report straight into the caller's pinned host buffer
+// (ckv_step.host_report): the last kernel of the step, launched behind the dense
+// pass as a programmatic dependent; griddepcontrol.wait orders it after every
+// earlier kernel of the step and makes their writes visible.
+struct PublishArgs {
+  const uint32_t* cert;
+  const int32_t* status;
+  const int32_t* ps;
+  const int32_t* en;
+  uint8_t* dst;
+  int32_t n_cert, n_ps, n_en;  // 4-byte words
+  int64_t off_status, off_ps, off_en;
+};
+
+__global__ void __launch_bounds__(256) k_publish(PublishArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t* d = reinterpret_cast<uint32_t*>(a.dst);
+  const int n = a.n_cert + 8 + a.n_ps + a.n_en;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i < a.n_cert) {
+      d[i] = __ldcg(a.cert + i);
+    } else if (i < a.n_cert + 8) {
+      const int j = i - a.n_cert;
+      reinterpret_cast<int32_t*>(a.dst + a.off_status)[j] = __ldcg(a.status + j);
+    } else if (i < a.n_cert + 8 + a.n_ps) {
+      const int j = i - a.n_cert - 8;
+      reinterpret_cast<int32_t*>(a.dst + a.off_ps)[j] = __ldcg(a.ps + j);
+    } else {
+      const int j = i - a.n_cert - 8 - a.n_ps;
+      reinterpret_cast<int32_t*>(a.dst + a.off_en)[j] = __ldcg(a.en + j);
+    }
+  }
+}
+
+cudaError_t launch_publish(const ckv_cache* c, const ckv_step* st, cudaStream_t s) {
+  int64_t lay[4];
+  report_layout(c->n_units, st->n_heads, lay);
+  PublishArgs a;
+  a.cert = reinterpret_cast<const uint32_t*>(st->cert);
+  a.status = c->status;
+  a.ps = st->page_stats;
+  a.en = st->explore_n;
+  a.dst = static_cast<uint8_t*>(st->host_report);
+  a.n_cert = (int32_t)((int64_t)c->n_units * st->n_heads * (int64_t)sizeof(ckv_cert) / 4);
+  a.n_ps = st->page_stats ? c->n_units * 4 : 0;
+  a.n_en = st->explore_n ? c->n_units * st->n_heads : 0;
+  a.off_status = lay[1];
+  a.off_ps = lay[2];
+  a.off_en = lay[3];
+  const int n = a.n_cert + 8 + a.n_ps + a.n_en;
+  const int grid = (n + 255) / 256 < dev_state().sms ? (n + 255) / 256 : dev_state().sms;
+  cudaError_t e = launch_k(true, k_publish, dim3(grid), dim3(256), 0, s, a);
+  g_launches += 1;
+  return e;
+}
+
 cudaError_t launch_group_flags(const ckv_cache* c, const ckv_step* st, cudaStream_t s) {
   DenseArgs a{*c, *st, 0, 0, 0, PageView{}};
   cudaMemsetAsync(st->group_flags, 0, sizeof(int32_t) * st->n_groups, s);

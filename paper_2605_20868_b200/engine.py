@@ -132,7 +132,6 @@ class CertifiedDecoder:
         st.ecap = max(1, int(round(0.05 * NB)) + 1)
         self.explore_n = torch.zeros((U, nh), dtype=torch.int32, device=dev)
         self.explore_pos = torch.zeros((U, nh, st.ecap), dtype=torch.int32, device=dev)
-        self.explore_n_host = torch.zeros((U, nh), dtype=torch.int32).pin_memory()
         self.rng_words = torch.zeros((16,), dtype=torch.int64, device=dev)
         self.rng_host = torch.zeros((16,), dtype=torch.int64).pin_memory()
         self.explore_work = torch.zeros((4 * U * nh + 64,), dtype=torch.int32, device=dev)
@@ -189,17 +188,33 @@ class CertifiedDecoder:
         self.scratch = scratch
         if scratch is not None:
             scratch.bind(cache, n_heads=self.nh, kcap=st.kcap)
-        self.cert_host = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8).pin_memory()
-        self.status_host = torch.zeros((8,), dtype=torch.int32).pin_memory()
-        self.ps_host = torch.zeros((U, 4), dtype=torch.int32).pin_memory()
+        # the step's bound report is written by its last kernel straight into pinned
+        # host memory (ckv_step.host_report): no device-to-host copies in the stream
+        self._report = self._report_buffer()
+        self.cert_host, self.status_host, self.ps_host, self.explore_n_host = self._report[1]
+
+    def _report_buffer(self):
+        """A pinned host_report buffer and its views (cert, status, page_stats,
+        explore_n) in the library's layout (ckv_report_layout)."""
+        U, nh = self.cache.n_units, self.nh
+        lay = (ctypes.c_int64 * 4)()
+        self.lib.ckv_report_layout(U, nh, lay)
+        buf = torch.zeros((int(lay[0]),), dtype=torch.uint8).pin_memory()
+        cert = buf[:U * nh * CERT_DTYPE.itemsize].view(U, nh, CERT_DTYPE.itemsize)
+        status = buf[lay[1]:lay[1] + 32].view(torch.int32)
+        ps = buf[lay[2]:lay[2] + U * 16].view(torch.int32).view(U, 4)
+        en = buf[lay[3]:lay[3] + U * nh * 4].view(torch.int32).view(U, nh)
+        return buf, (cert, status, ps, en)
 
     # -- the device step -----------------------------------------------------
-    def launch(self, queries=None, reduce_flags=None, explore=False):
+    def launch(self, queries=None, reduce_flags=None, explore=False, report=None):
         """Enqueue the whole step (no host sync); returns immediately.
 
         ``reduce_flags(group_flags)`` -- e.g. an all-reduce(MAX) across the
         ranks of a KV-head sharded job -- runs between the Rung-4 requests and
-        their resolution, in stream order (ckv_decode_flags / _finish)."""
+        their resolution, in stream order (ckv_decode_flags / _finish).
+        ``report``: a pinned buffer from ``_report_buffer`` the step's last kernel
+        writes the bound report into (None: the report stays on the device)."""
         if queries is not None:
             self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
         sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
@@ -209,6 +224,7 @@ class CertifiedDecoder:
         # exploration: samples drawn on the device from the generator state in rng_words
         self.st.explore_rng = _ptr(self.rng_words) if explore else None
         self.st.explore_n = _ptr(self.explore_n) if explore else None
+        self.st.host_report = report.data_ptr() if report is not None else None
         if reduce_flags is None:
             _lib.check(self.lib.ckv_decode_step(*args, sc, nbk, stream), "ckv_decode_step")
             return
@@ -235,7 +251,7 @@ class CertifiedDecoder:
         explore = self.policy.exploration_rate > 0 and rng is not None
         if explore and self._attached is None:
             self._rng_upload(rng)
-        self.launch(queries, explore=explore or self._attached is not None)
+        self.launch(queries, explore=explore or self._attached is not None, report=self._report[0])
         out = self._finish(explore or self._attached is not None)
         if explore and self._attached is None:
             self._rng_download(rng)
@@ -281,26 +297,15 @@ class CertifiedDecoder:
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
         explore = self._attached is not None
-        self.launch(queries, reduce_flags, explore=explore)
         k = self._ring_i = (getattr(self, "_ring_i", 1) + 1) % 2
         if not hasattr(self, "_ring"):
-            shp = self.cert_host.shape
-            self._ring = [(torch.zeros(shp, dtype=torch.uint8).pin_memory(),
-                           torch.zeros((8,), dtype=torch.int32).pin_memory(),
-                           torch.zeros(self.ps_host.shape, dtype=torch.int32).pin_memory(),
-                           torch.zeros(self.explore_n.shape, dtype=torch.int32).pin_memory(),
-                           torch.cuda.Event()) for _ in range(2)]
+            self._ring = [self._report_buffer() + (torch.cuda.Event(),) for _ in range(2)]
             self._ring_pending = [None, None]
         prev = self._ring_pending[k]
         if prev is not None:
-            prev._decode()  # decode the step that last used this buffer before reusing it
-        cert_h, stat_h, ps_h, en_h, ev = self._ring[k]
-        cert_h.copy_(self.cert_buf, non_blocking=True)
-        stat_h.copy_(self.cache.status, non_blocking=True)
-        if self.scratch is not None:
-            ps_h.copy_(self.page_stats, non_blocking=True)
-        if explore:
-            en_h.copy_(self.explore_n, non_blocking=True)
+            prev._decode()  # the step that last used this report buffer, before it is rewritten
+        buf, (cert_h, stat_h, ps_h, en_h), ev = self._ring[k]
+        self.launch(queries, reduce_flags, explore=explore, report=buf)
         ev.record(torch.cuda.current_stream(self.cache.device))
         pend = PendingStep(self, cert_h, stat_h, ps_h, ev, self.cache.num_tokens,
                            en_h if explore else None)
@@ -308,12 +313,7 @@ class CertifiedDecoder:
         return pend
 
     def _finish(self, explore=False):
-        self.cert_host.copy_(self.cert_buf, non_blocking=True)
-        self.status_host.copy_(self.cache.status, non_blocking=True)
-        if self.scratch is not None:
-            self.ps_host.copy_(self.page_stats, non_blocking=True)
-        if explore:
-            self.explore_n_host.copy_(self.explore_n, non_blocking=True)
+        # the step's last kernel wrote the report into self._report (host_report)
         torch.cuda.current_stream(self.cache.device).synchronize()  # the step's only host sync
         return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens,
                             self.explore_n_host if explore else None)
