@@ -194,9 +194,7 @@ static ckv_status decode_begin(const ckv_cache* c, const ckv_policy* pol, ckv_st
   if (!step_ok(c, pol, st, host_max_blocks)) return CKV_EINVAL;
   if (scratch && (!st->page_stats || !scratch->key_lru || !scratch->value_lru || !scratch->counters))
     return CKV_EINVAL;
-  // Tier-2 loss is reported per step
-  cudaError_t e = cudaMemsetAsync(c->status + CKV_ST_TIER2, 0, sizeof(int32_t), S(stream));
-  if (e != cudaSuccess) return st_of(e);
+  // (the per-step words -- Tier-2 loss, page stats -- are cleared by k_step_begin)
   return st_of(ckv::launch_decode(c, pol, st, scratch, host_max_blocks, finish, S(stream)));
 }
 

@@ -978,6 +978,15 @@ __global__ void k_fused_attend(const float* s, const float* v, const int64_t* bn
   }
 }
 
+// Clears the step's per-step status words before its kernels run: the Tier-2
+// loss flag and (fused LRU accounting) the per-unit page stats.  A programmatic
+// dependent of the previous kernel on the stream (which may still read them).
+__global__ void k_step_begin(int32_t* status, int32_t* ps, int n_ps) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) status[CKV_ST_TIER2] = 0;
+  for (int i = threadIdx.x; i < n_ps; i += blockDim.x) ps[i] = 0;
+}
+
 // =============================================================================
 // launchers
 // =============================================================================
@@ -1136,8 +1145,12 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
   const int nsplit_used = min(nsplit, host_max_blocks);
   cudaStream_t s2 = (nch > 1) ? dev_state().tail : s;
   cudaError_t e = cudaSuccess;
-  if (sc && lru_fused(c, sc))
-    cudaMemsetAsync(st->page_stats, 0, sizeof(int32_t) * 4 * (size_t)U, s);
+  {  // the step's per-step words: Tier-2 loss (reported per step), the fused LRU's page stats
+    int32_t* ps = (sc && lru_fused(c, sc)) ? st->page_stats : nullptr;
+    e = launch_k(true, k_step_begin, dim3(1), dim3(256), 0, s, c->status, ps, ps ? 4 * U : 0);
+    ++g_launches;
+    if (e != cudaSuccess) return e;
+  }
   // the kernel dataflow needs the selection to build the union list and one
   // unit chunk per step (the chunked overlap puts events between the kernels)
   ckv_step stf = *st;
@@ -1151,8 +1164,12 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
     if (nu <= 0) break;
     StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
     if (nsplit_used > 0 || st->flow) {  // with the dataflow every unit's pass A must publish
-      k_pass_a<<<dim3(max(nsplit_used, 1), nu), PA_WARPS * 32, smA, s>>>(a);
+      // behind k_step_begin (k == 0, no event in between) as a programmatic dependent:
+      // that kernel does not trigger early, so pass A starts when it has finished
+      const bool pdl = k == 0 && !st->prof_begin;
+      e = launch_k(pdl, k_pass_a, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32), smA, s, a);
       ++g_launches;
+      if (e != cudaSuccess) break;
     }
     if (k == nch - 1 || u0 + nu >= U) {
       if (st->prof_end) cudaEventRecord(reinterpret_cast<cudaEvent_t>(st->prof_end), s);

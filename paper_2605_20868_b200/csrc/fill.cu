@@ -218,6 +218,9 @@ __global__ void __launch_bounds__(128) k_fill(FillArgs a) {
 // lengths and v_max, or, if any token was non-finite, counts the rejection and
 // commits nothing (same effect as k_check_finite + k_fill + k_tail).
 __global__ void __launch_bounds__(128) k_append1(FillArgs a) {
+  // a programmatic dependent of whatever ran before it on the stream (the step's
+  // report kernel): its launch is staged early, its work waits for that to finish
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const ckv_cache& c = a.c;
   const int u = blockIdx.x, tid = threadIdx.x;
   const uint16_t kb = a.k_new[(size_t)u * D + tid], vb = a.v_new[(size_t)u * D + tid];
@@ -347,9 +350,9 @@ cudaError_t launch_append(const ckv_cache* c, const uint16_t* k_new, const uint1
   g_launches = 0;
   if (n_tok == 1) {  // the decode step's append: one launch
     FillArgs a{*c, k_new, v_new, 1};
-    k_append1<<<c->n_units, 128, 0, s>>>(a);
+    cudaError_t e = launch_k(true, k_append1, dim3(c->n_units), dim3(128), 0, s, a);
     ++g_launches;
-    return cudaGetLastError();
+    return e;
   }
   size_t n16 = (size_t)c->n_units * n_tok * D / 8;
   int grid = (int)((n16 + 255) / 256);

@@ -216,7 +216,18 @@ class CertifiedDecoder:
         ``report``: a pinned buffer from ``_report_buffer`` the step's last kernel
         writes the bound report into (None: the report stays on the device)."""
         if queries is not None:
-            self.q.copy_(torch.as_tensor(queries).reshape(self.q.shape), non_blocking=True)
+            qt = queries if isinstance(queries, torch.Tensor) else torch.as_tensor(queries)
+            if (qt.device == self.q.device and qt.dtype == torch.float64 and qt.is_contiguous()
+                    and qt.numel() == self.q.numel()):
+                # a device float64 query tensor is read in place (no copy kernel in the
+                # step's stream); it must stay alive until the step has run, as any
+                # tensor handed to an enqueued kernel
+                self.st.q = qt.data_ptr()
+            else:
+                self.q.copy_(qt.reshape(self.q.shape), non_blocking=True)
+                self.st.q = self.q.data_ptr()
+        else:  # the caller filled self.q
+            self.st.q = self.q.data_ptr()
         sc = ctypes.byref(self.scratch.c) if self.scratch is not None else None
         args = (ctypes.byref(self.cache.c), ctypes.byref(self.pol_c), ctypes.byref(self.st))
         nbk, stream = self.cache.num_blocks, _stream(self.cache.device)
