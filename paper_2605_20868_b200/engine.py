@@ -58,8 +58,8 @@ class StepOutput:
 class PendingStep:
     """Handle of a step enqueued by ``CertifiedDecoder.step_async``."""
 
-    def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens, en_h=None):
-        self._args = (cert_h, stat_h, ps_h, n_tokens, en_h)
+    def __init__(self, dec, cert_h, stat_h, ps_h, event, n_tokens, en_h=None, out=None):
+        self._args = (cert_h, stat_h, ps_h, n_tokens, en_h, out)
         self._dec, self._ev, self._res, self._exc = dec, event, None, None
 
     def done(self):
@@ -111,7 +111,7 @@ class CertifiedDecoder:
         st.dense_splits = int(dense_splits)
         U, NB, nh, dev = cache.n_units, cache.max_blocks, self.nh, cache.device
         self.q = torch.zeros((U, nh, D), dtype=torch.float64, device=dev)
-        self.out = torch.zeros((U, nh, D), dtype=torch.float32, device=dev)
+        self.out = self._out0 = torch.zeros((U, nh, D), dtype=torch.float32, device=dev)
         self.cert_buf = torch.zeros((U, nh, CERT_DTYPE.itemsize), dtype=torch.uint8, device=dev)
         self.lm1 = torch.zeros((U, nh, NB), dtype=torch.float32, device=dev)
         self.split_state = torch.zeros((U, st.n_splits, 4, _lib.SPLIT_FLOATS),
@@ -207,14 +207,24 @@ class CertifiedDecoder:
         return buf, (cert, status, ps, en)
 
     # -- the device step -----------------------------------------------------
-    def launch(self, queries=None, reduce_flags=None, explore=False, report=None):
+    def launch(self, queries=None, reduce_flags=None, explore=False, report=None, out=None):
         """Enqueue the whole step (no host sync); returns immediately.
 
         ``reduce_flags(group_flags)`` -- e.g. an all-reduce(MAX) across the
         ranks of a KV-head sharded job -- runs between the Rung-4 requests and
         their resolution, in stream order (ckv_decode_flags / _finish).
         ``report``: a pinned buffer from ``_report_buffer`` the step's last kernel
-        writes the bound report into (None: the report stays on the device)."""
+        writes the bound report into (None: the report stays on the device).
+        ``out``: the device tensor the outputs go to (None: ``self._out0``);
+        ``self.out`` names the latest step's."""
+        if out is None:
+            out = self._out0
+        elif (out.device != self._out0.device or out.dtype != torch.float32
+              or out.shape != self._out0.shape or not out.is_contiguous()):
+            raise ValueError("out must be a contiguous float32 device tensor of shape "
+                             f"{tuple(self._out0.shape)}")
+        self.out = out
+        self.st.out = out.data_ptr()
         if queries is not None:
             qt = queries if isinstance(queries, torch.Tensor) else torch.as_tensor(queries)
             if (qt.device == self.q.device and qt.dtype == torch.float64 and qt.is_contiguous()
@@ -297,14 +307,16 @@ class CertifiedDecoder:
             self._rng_download(rng)
         return rng
 
-    def step_async(self, queries, reduce_flags=None):
+    def step_async(self, queries, reduce_flags=None, out=None):
         """Enqueue a certified step and return a ``PendingStep`` without a host
-        sync: the certificate array is copied into one of two pinned buffers
-        behind the step's kernels, so the host can read step i's bound report
-        while the device runs step i+1.  The output stays on the device
-        (``self.out``, valid in stream order until the next step overwrites
-        it); dense rungs are already applied there.  Exploration runs when a
-        generator is attached (``attach_rng``)."""
+        sync: the step's last kernel writes its bound report into one of two
+        pinned buffers, so the host can read step i's report while the device
+        runs step i+1.  The output stays on the device, dense rungs already
+        applied: in ``out`` (a float32 device tensor [U, n_heads, 128] of the
+        caller, e.g. one of two buffers that leave for the host while the next
+        step runs) or in the decoder's own ``self.out``, valid in stream order
+        until the next step overwrites it.  Exploration runs when a generator
+        is attached (``attach_rng``)."""
         if self.cache.num_tokens == 0:
             raise EmptyCacheError("cannot attend over an empty cache")
         explore = self._attached is not None
@@ -316,10 +328,10 @@ class CertifiedDecoder:
         if prev is not None:
             prev._decode()  # the step that last used this report buffer, before it is rewritten
         buf, (cert_h, stat_h, ps_h, en_h), ev = self._ring[k]
-        self.launch(queries, reduce_flags, explore=explore, report=buf)
+        self.launch(queries, reduce_flags, explore=explore, report=buf, out=out)
         ev.record(torch.cuda.current_stream(self.cache.device))
         pend = PendingStep(self, cert_h, stat_h, ps_h, ev, self.cache.num_tokens,
-                           en_h if explore else None)
+                           en_h if explore else None, self.out)
         self._ring_pending[k] = pend
         return pend
 
@@ -329,7 +341,7 @@ class CertifiedDecoder:
         return self._output(self.cert_host, self.status_host, self.ps_host, self.cache.num_tokens,
                             self.explore_n_host if explore else None)
 
-    def _output(self, cert_h, stat_h, ps_h, n_tokens, en_h=None):
+    def _output(self, cert_h, stat_h, ps_h, n_tokens, en_h=None, out_t=None):
         if self.cache.take_rejections(stat_h):  # a deferred append check (DeviceKVCache.append)
             self.cache.resync()
             raise ValueError("non-finite key/value entry (append rejected on the device)")
@@ -342,7 +354,7 @@ class CertifiedDecoder:
         n_units = int(np.isin(self.unit_group_host, flagged).sum()) if flagged.size else 0
         staging = n_units * 2 * n_tokens * D * 2
         ps = ps_h.numpy().copy() if self.scratch is not None else None
-        out = StepOutput(self.out, cert, kinds, ps, staging, self)
+        out = StepOutput(self.out if out_t is None else out_t, cert, kinds, ps, staging, self)
         if en_h is not None:
             out.explore_counts = en_h.numpy().copy()
         return out
