@@ -29,27 +29,35 @@ namespace ckv {
 #ifndef PA_WARPS_CFG
 #define PA_WARPS_CFG 4
 #endif
-#ifndef PA_STAGES_CFG
-#define PA_STAGES_CFG 2
-#endif
 constexpr int PA_WARPS = PA_WARPS_CFG;
-constexpr int PA_STAGES = PA_STAGES_CFG;
 
+// A warp's ring refills a stage only after computing on it, so a record costs
+// (latency + compute) / stages.  Long splits (C3: 512 blocks per CTA) run three
+// stages (1.4% faster pass A there); short ones (the kv1 proxy: ~220) two, where
+// the three-stage prologue costs more than it hides.  4 CTAs x 56.4 KB per SM
+// fit only with q' staged in the last warp's last stage, which is filled once
+// the fragments are built.
+template <int STG>
 struct PassASmem {
-  uint8_t stage[PA_WARPS][PA_STAGES][REC];
-  uint64_t bar[PA_WARPS][PA_STAGES];
-  float qh[H * D];
+  static constexpr bool QALIAS = STG >= 3;
+  uint8_t stage[PA_WARPS][STG][REC];
+  uint64_t bar[PA_WARPS][STG];
   float pbuf[PA_WARPS][H][B];  // p' of the block, tokens permuted (vmeta order)
+  float qh[QALIAS ? 1 : H * D];
 };
+static_assert(H * D * 4 <= REC, "q' staging fits one stage");
+constexpr int PA_LONG_SPLIT = 384;  // blocks per CTA from which three stages pay
 
 // (PVFrag / pv_frag / pv_block_sub: step.cuh)
 
 #ifndef PA_MINB
 #define PA_MINB 4
 #endif
+template <int PA_STAGES>
 __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  PassASmem& S = *reinterpret_cast<PassASmem*>(smem_raw);
+  using Smem = PassASmem<PA_STAGES>;
+  Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const ckv_cache& c = a.c;
   const ckv_step& st = a.st;
   TraceScope trace_(st.trace, CKV_TR_PASS_A);
@@ -69,10 +77,11 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
   const int b0 = (int)((long long)sp * nb / nsp);
   const int b1 = (int)((long long)(sp + 1) * nb / nsp);
 
+  float* qh = Smem::QALIAS ? reinterpret_cast<float*>(S.stage[PA_WARPS - 1][PA_STAGES - 1]) : S.qh;
   for (int i = tid; i < H * D; i += blockDim.x) {
     int h = i / D;
-    S.qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845)
-                       : 0.f;
+    qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845)
+                     : 0.f;
   }
   if (tid == 0) {
     for (int w = 0; w < PA_WARPS; ++w)
@@ -80,9 +89,6 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
-
-  QFrag f;
-  load_qfrag(f, S.qh, lane);
 
   const int span = b1 - b0;
   const int nmine = (span > warp) ? (span - warp + PA_WARPS - 1) / PA_WARPS : 0;
@@ -96,12 +102,26 @@ __global__ void __launch_bounds__(PA_WARPS * 32, PA_MINB) k_pass_a(StepArgs a) {
 #else
 #define PA_G2S(dst, src, bar) bulk_g2s(dst, src, REC, bar)
 #endif
+  // the ring's first copies (all but the stage holding q'), then the fragments
+  const bool last_w = warp == PA_WARPS - 1;
   if (lane == 0) {
     for (int s = 0; s < PA_STAGES && s < nmine; ++s) {
+      if (Smem::QALIAS && last_w && s == PA_STAGES - 1) break;
       int b = b0 + warp + PA_WARPS * s;
       mbar_expect_tx(&S.bar[warp][s], REC);
       PA_G2S(S.stage[warp][s], ubase + (size_t)b * REC, &S.bar[warp][s]);
     }
+  }
+  QFrag f;
+  load_qfrag(f, qh, lane);
+  if (Smem::QALIAS) {
+    fence_proxy_async();  // q' (generic writes) before the bulk copy that overwrites it
+    __syncthreads();
+  }
+  if (Smem::QALIAS && last_w && lane == 0 && PA_STAGES - 1 < nmine) {
+    const int s = PA_STAGES - 1;
+    mbar_expect_tx(&S.bar[warp][s], REC);
+    PA_G2S(S.stage[warp][s], ubase + (size_t)(b0 + warp + PA_WARPS * s) * REC, &S.bar[warp][s]);
   }
 
   const int h = lane & 3;
@@ -1121,8 +1141,8 @@ bool decode_flow(const ckv_cache* c, const ckv_step* st) {
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                           const ckv_scratch* sc, int host_max_blocks, bool finish, cudaStream_t s) {
   g_launches = 0;
-  const size_t smA = sizeof(PassASmem);
-  set_max_dyn_smem(k_pass_a, (int)smA);
+  set_max_dyn_smem(k_pass_a<2>, (int)sizeof(PassASmem<2>));
+  set_max_dyn_smem(k_pass_a<3>, (int)sizeof(PassASmem<3>));
   {
     const int smS = (int)(sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4);
     set_max_dyn_smem(k_select<8, 1024>, smS);
@@ -1167,7 +1187,13 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
       // behind k_step_begin (k == 0, no event in between) as a programmatic dependent:
       // that kernel does not trigger early, so pass A starts when it has finished
       const bool pdl = k == 0 && !st->prof_begin;
-      e = launch_k(pdl, k_pass_a, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32), smA, s, a);
+      const bool long_split = nsplit_used > 0 && host_max_blocks / nsplit_used >= PA_LONG_SPLIT;
+      if (long_split)
+        e = launch_k(pdl, k_pass_a<3>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32),
+                     sizeof(PassASmem<3>), s, a);
+      else
+        e = launch_k(pdl, k_pass_a<2>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32),
+                     sizeof(PassASmem<2>), s, a);
       ++g_launches;
       if (e != cudaSuccess) break;
     }
