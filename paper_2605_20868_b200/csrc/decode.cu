@@ -32,9 +32,9 @@ namespace ckv {
 constexpr int PA_WARPS = PA_WARPS_CFG;
 
 // A warp's ring refills a stage only after computing on it, so a record costs
-// (latency + compute) / stages.  Long splits (C3: 512 blocks per CTA) run three
-// stages (1.4% faster pass A there); short ones (the kv1 proxy: ~220) two, where
-// the three-stage prologue costs more than it hides.  4 CTAs x 56.4 KB per SM
+// (latency + compute) / stages.  Many waves of CTAs (C3: 16) run three stages
+// (1.4% faster pass A there); a few (the kv1 proxy: 2) two, where three measured
+// 4% slower.  4 CTAs x 56.4 KB per SM
 // fit only with q' staged in the last warp's last stage, which is filled once
 // the fragments are built.
 template <int STG>
@@ -46,7 +46,7 @@ struct PassASmem {
   float qh[QALIAS ? 1 : H * D];
 };
 static_assert(H * D * 4 <= REC, "q' staging fits one stage");
-constexpr int PA_LONG_SPLIT = 384;  // blocks per CTA from which three stages pay
+constexpr int PA_DEEP_WAVES = 4;  // waves of CTAs from which three stages pay
 
 // (PVFrag / pv_frag / pv_block_sub: step.cuh)
 
@@ -1187,8 +1187,8 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
       // behind k_step_begin (k == 0, no event in between) as a programmatic dependent:
       // that kernel does not trigger early, so pass A starts when it has finished
       const bool pdl = k == 0 && !st->prof_begin;
-      const bool long_split = nsplit_used > 0 && host_max_blocks / nsplit_used >= PA_LONG_SPLIT;
-      if (long_split)
+      const long long ctas = (long long)max(nsplit_used, 1) * nu;
+      if (ctas >= PA_DEEP_WAVES * (long long)dev_state().sms * PA_MINB)
         e = launch_k(pdl, k_pass_a<3>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32),
                      sizeof(PassASmem<3>), s, a);
       else
