@@ -459,6 +459,9 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
         for ev in ev_used + ev_d2h:
             ev.record(comp)
         ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(E)]
+        esampler = ClockSampler(local, dev) if (rank == 0 and clocks_wanted) else None
+        if esampler:
+            esampler.start()
         torch.cuda.synchronize()
         e0 = time.perf_counter()
         prev = None
@@ -507,6 +510,8 @@ def run_gpu(args, ck, dev, world, rank, local, K, W, dist, total_units, e2e_want
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms, "steps": E}
         if not serial:  # the device's own step interval inside this loop (diagnostic)
             e2e["device_ms_per_step"] = ev_step[0].elapsed_time(ev_step[E - 1]) / (E - 1)
+        if esampler:  # E steps back to back run long enough to meet the board's power cap
+            e2e["clocks"] = esampler.stop()
 
     return dict(ms=ms, pa_ms=pa_ms, clocks=clocks, n_launch=n_launch, n_dense=n_dense,
                 stats=stats, last=last, dec=dec, cache=cache, scratch=scratch, e2e=e2e,
