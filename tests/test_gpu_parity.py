@@ -492,6 +492,52 @@ def test_step_async_matches_step_and_defers_append_check(ck):
     assert ca.num_tokens == t0 + 1
 
 
+def test_step_async_out_buffers_and_host_report(ck):
+    """The serving-loop path -- bound report written into pinned host memory by the
+    step's last kernel, outputs into caller buffers (out=), device float64 queries
+    read in place -- equals the synchronous step bit for bit: outputs,
+    certificates, page statistics; the report's certificates equal the device
+    certificate array; float32 / host queries (the copy path) give the same."""
+    rng = np.random.default_rng(22)
+    U, n = 5, 2100
+    k = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    v = torch.from_numpy(rng.standard_normal((U, n, 128))).half().cuda()
+    ca, cb = ck.DeviceKVCache(U, n + 32), ck.DeviceKVCache(U, n + 32)
+    ca.append(k, v)
+    cb.append(k, v)
+    pol = ck.PolicyConfig(exploration_rate=0.0, k_max=12)
+    da = ck.CertifiedDecoder(ca, pol, n_heads=4, scratch=ck.ScratchCache(ca.max_blocks))
+    db = ck.CertifiedDecoder(cb, pol, n_heads=4, scratch=ck.ScratchCache(cb.max_blocks))
+    od = [torch.full((U, 4, 128), float("nan"), device="cuda") for _ in range(2)]
+    kn = torch.from_numpy(rng.standard_normal((6, U, 1, 128))).half().cuda()
+    for i in range(6):
+        q = torch.from_numpy(rng.standard_normal((U, 4, 128))).cuda()
+        pa = da.step_async(q, out=od[i % 2])
+        if i % 2 == 0:  # the copy path: host data, or a strided device view
+            qb = q.cpu().numpy()
+        else:
+            qw = torch.zeros((U, 4, 256), dtype=torch.float64, device="cuda")
+            qw[..., ::2] = q
+            qb = qw[..., ::2]
+        rb = db.step(qb)
+        ra = pa.result()
+        assert ra.out.data_ptr() == od[i % 2].data_ptr()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(ra.cert, rb.cert)
+        np.testing.assert_array_equal(ra.page_stats, rb.page_stats)
+        assert torch.equal(od[i % 2], db.out)
+        rep = da.cert_buf.cpu().numpy().view(ck.engine.CERT_DTYPE).reshape(U, 4)
+        np.testing.assert_array_equal(ra.cert, rep)
+        ca.append(kn[i], kn[i], validate=False)
+        cb.append(kn[i], kn[i], validate=False)
+    # the float32 query (copy path) on the async side too
+    q = torch.from_numpy(rng.standard_normal((U, 4, 128))).cuda()
+    ra = da.step_async(q.float()).result()
+    rb = db.step(q.float())
+    np.testing.assert_array_equal(ra.cert, rb.cert)
+    assert torch.equal(da.out, db.out)
+
+
 @pytest.mark.parametrize("env", [{"CKV_NO_STASH": "1"}, {"CKV_CHUNKS": "2"}, {"CKV_SEPARATE_LRU": "1"},
                                  {"CKV_SEPARATE_UNION": "1"}],
                          ids=["no_stash", "chunks2", "separate_lru", "separate_union"])
