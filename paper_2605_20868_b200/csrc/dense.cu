@@ -212,25 +212,7 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
     dense_split_done(a, item, mscratch);
     continue;
   }
-  for (int i = tid; i < H * D; i += blockDim.x) {
-    const int h = i / D;
-    S.qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845) : 0.f;
-  }
-  // Tier-2 must hold every block we read (cache.py:138-142)
-  for (int b = b0 + tid; b < b1; b += blockDim.x)
-    if (!c.tier2_valid[(size_t)u * c.max_blocks + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
-  __syncthreads();
-  QFrag16 f16;
-  load_qfrag16(f16, S.qh, lane);
-  const int h = lane & 3, t0 = lane >> 2;
-  const int pi0 = 4 * (t0 >> 1) + (t0 & 1), pi1 = pi0 + 2;
-  const int hb = lane >> 3;
-  const bool lo_lane = (lane >> 2) & 1;
   const size_t ubk = (size_t)u * c.max_blocks;
-  float m_h = dninf(), l_h = 0.f;
-  float acc[NG][4];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
   // a block already paged into an HBM slot this or an earlier step (its bytes are
   // the Tier-2 bytes) is read from the slot instead of over PCIe from host Tier-2
   const PageView& pv = a.pv;
@@ -248,8 +230,26 @@ __global__ void __launch_bounds__(DN_WARPS * 32) k_dense(DenseArgs a_in) {
     bulk_g2s(S.stg[warp][s2][0], ks, B * D * 2, &S.bar[warp][s2]);
     bulk_g2s(S.stg[warp][s2][1], vs, B * D * 2, &S.bar[warp][s2]);
   };
-  if (lane == 0)
+  if (lane == 0)  // the ring's first copies, before the query setup they do not need
     for (int i = 0; i < DN_STAGES && i < nmine; ++i) issue(i);
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    const int h = i / D;
+    S.qh[i] = (h < nh) ? (float)(st.q[((size_t)u * nh + h) * D + (i % D)] * 0.08838834764831845) : 0.f;
+  }
+  // Tier-2 must hold every block we read (cache.py:138-142)
+  for (int b = b0 + tid; b < b1; b += blockDim.x)
+    if (!c.tier2_valid[(size_t)u * c.max_blocks + b]) atomicOr(&c.status[CKV_ST_TIER2], 1);
+  __syncthreads();
+  QFrag16 f16;
+  load_qfrag16(f16, S.qh, lane);
+  const int h = lane & 3, t0 = lane >> 2;
+  const int pi0 = 4 * (t0 >> 1) + (t0 & 1), pi1 = pi0 + 2;
+  const int hb = lane >> 3;
+  const bool lo_lane = (lane >> 2) & 1;
+  float m_h = dninf(), l_h = 0.f;
+  float acc[NG][4];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
   for (int i = 0; i < nmine; ++i) {
     const int s2 = (kb + i) % DN_STAGES;
     mbar_wait(&S.bar[warp][s2], (uint32_t)((kb + i) / DN_STAGES) & 1u);

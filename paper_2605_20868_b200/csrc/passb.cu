@@ -74,17 +74,6 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
     if (tid < H) cs[tid * CKV_CHUNK_FLOATS] = ninf();
     return;
   }
-  __syncthreads();  // the previous chunk's reduction is done with S
-  for (int i = tid; i < H * D; i += blockDim.x) {
-    const int hh = i / D;
-    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
-                        : 0.f;
-  }
-  __syncthreads();
-  QFrag f;
-  load_qfrag(f, S.qh, lane);
-  QFrag16 f16;
-  load_qfrag16(f16, S.qh, lane);
 
   const int h = lane & 3;  // the head this lane's scores belong to
   const int hq = (h < nh) ? h : 0;
@@ -228,10 +217,22 @@ __device__ __forceinline__ void pass_b_chunk(const StepArgs& a, PassBSmem& S, co
       bulk_g2s(S.kt[warp][stg], src, B * D * 2, &S.bar[warp][stg]);
     }
   };
+  // the item metadata first: its two dependent load rounds overlap the query setup
   load_e(0, 0);
   load_e(1, 32);
   load_words(0);
   load_words(1);
+  __syncthreads();  // the previous chunk's reduction is done with S
+  for (int i = tid; i < H * D; i += blockDim.x) {
+    const int hh = i / D;
+    S.qh[i] = (hh < nh) ? (float)(st.q[((size_t)u * nh + hh) * D + (i % D)] * 0.08838834764831845)
+                        : 0.f;
+  }
+  __syncthreads();
+  QFrag f;
+  load_qfrag(f, S.qh, lane);
+  QFrag16 f16;
+  load_qfrag16(f16, S.qh, lane);
   int cur = item_at(0);
   int i1 = item_at(1);
   Meta mc = fetch(0);
