@@ -230,11 +230,10 @@ class CertifiedDecoder:
             if (qt.device == self.q.device and qt.dtype == torch.float64 and qt.is_contiguous()
                     and qt.numel() == self.q.numel()):
                 # a device float64 query tensor is read in place (no copy kernel in the
-                # step's stream); the decoder keeps it alive until the next step (a
-                # temporary allocated on another stream would otherwise be reusable
-                # before the step has read it)
+                # step's stream); record_stream keeps the allocator from reusing it
+                # before the step has read it, whichever stream allocated it
                 self.st.q = qt.data_ptr()
-                self._q_keep = qt
+                qt.record_stream(torch.cuda.current_stream(self.cache.device))
             else:
                 self.q.copy_(qt.reshape(self.q.shape), non_blocking=True)
                 self.st.q = self.q.data_ptr()
