@@ -147,15 +147,20 @@ def test_device_vs_oracle_narrow(ck, name):
             assert drec["rung4_staging_bytes"] == orec["rung4_staging_bytes"]
 
 
-# ---- sampled units at the C2 / C3 / C5 shapes --------------------------------------
+# ---- sampled units at the C2 / C3 / C4 / C5 shapes ---------------------------------
 
-SHAPES = {"c2": (32768, False), "c3": (131072, False), "c5": (65536, True)}
+# name: (context, adversarial, Tier-2 placement, v_tol).  C4 runs one sequence of its
+# batch of 32 (256 units): 16K context, Tier-2 in pinned host RAM behind a scratch
+# that holds every block (misses paged in by pass B), the tight v_tol that makes
+# Rung 2 promote values.
+SHAPES = {"c2": (32768, False, "device", None), "c3": (131072, False, "device", None),
+          "c4": (16384, False, "host", 1e-3), "c5": (65536, True, "device", None)}
 LAYERS, KV_HEADS, NH = 32, 8, 4
 
 
-def _build(ck, ctx, adversarial, seed=77):
+def _build(ck, ctx, adversarial, seed=77, tier2="device"):
     U = LAYERS * KV_HEADS
-    cache = ck.DeviceKVCache(U, ctx + 64)
+    cache = ck.DeviceKVCache(U, ctx + 64, tier2=tier2)
     g = torch.Generator(device="cuda").manual_seed(seed)
     chunk = max(16, min(4096, (1 << 22) // U))
     for pos in range(0, ctx, chunk):  # the bench's prefill recipe (bench.py)
@@ -182,14 +187,20 @@ def _build(ck, ctx, adversarial, seed=77):
 @pytest.mark.parametrize("name", sorted(SHAPES))
 def test_sampled_units_at_baseline_shape(ck, name):
     from paper_2605_20868_b200 import _lib
-    ctx, adversarial = SHAPES[name]
-    cache, q, faults = _build(ck, ctx, adversarial)
+    ctx, adversarial, tier2, v_tol = SHAPES[name]
+    cache, q, faults = _build(ck, ctx, adversarial, tier2=tier2)
     U = cache.n_units
     groups = np.arange(U) % LAYERS  # kv-major units: step-wide Rung 4 per layer
-    pol = ck.PolicyConfig(exploration_rate=0.0)
-    opol = OraclePolicy(exploration_rate=0.0)
-    dec = ck.CertifiedDecoder(cache, pol, n_heads=NH, rung4_group=groups)
+    vkw = {} if v_tol is None else {"v_tol": v_tol}
+    pol = ck.PolicyConfig(exploration_rate=0.0, **vkw)
+    opol = OraclePolicy(exploration_rate=0.0, **vkw)
+    scratch = ck.ScratchCache(cache.max_blocks) if tier2 == "host" else None
+    dec = ck.CertifiedDecoder(cache, pol, n_heads=NH, rung4_group=groups, scratch=scratch)
     res = dec.step(q)
+    if v_tol is not None:  # the tight v_tol promotes values somewhere in the step
+        assert int(res.cert["n_value_promoted"].sum()) > 0
+    if tier2 == "host":  # every promoted block was paged into its HBM slot
+        assert int(res.page_stats[:, 1].sum()) > 0
     out = res.out.double().cpu().numpy()
     # the step-wide resolution against the device's own per-head requests
     r4 = np.array([[bool(int(res.cert[u, h]["flags"]) & (_lib.F_CANARY | _lib.F_NUMERIC))
@@ -201,6 +212,8 @@ def test_sampled_units_at_baseline_shape(ck, name):
     sample = set(int(u) for u in rs.choice(U, 2, replace=False))
     own_r3 = [int(u) for u in np.nonzero((res.kinds == 1).any(1))[0]]
     sample |= set(own_r3[:2])
+    vprom = [int(u) for u in np.nonzero((res.cert["n_value_promoted"] > 0).any(1))[0]]
+    sample |= set(vprom[:2])  # units whose heads promote values (C4's tight v_tol)
     if adversarial:
         assert layer_r4[0] and not layer_r4[1:].any()
         sample |= {0, LAYERS}  # the corrupted unit and another KV head of layer 0
@@ -225,6 +238,6 @@ def test_sampled_units_at_baseline_shape(ck, name):
             ref = oracle_row(r, kind, o_ref)
             ref["vscale"] = vscale
             compare(rep, f"unit {u} head {h}", d, ref, margins_from_oracle(r, opol), tol, num)
-    del dec, cache
+    del dec, cache, scratch
     torch.cuda.empty_cache()
     _finish(rep)
