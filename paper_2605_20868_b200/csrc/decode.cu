@@ -341,11 +341,11 @@ __device__ __forceinline__ float2 block_max_f2(float a, float b, float* red) {
   return make_float2(ta, tb);
 }
 
+// The small fields first, then the arrays; the radix histogram and the coverage
+// prefix are live in different phases and share storage.  The union builder at
+// the end (last q-head CTA of a unit) uses everything from `big` on as its bitmap
+// scratch: sel_body_bytes() sizes the dynamic allocation for it.
 struct SelSmem {
-  int hist[2048];                         // radix-select histogram
-  unsigned long long cand[SEL_MAXSORT];   // candidates (block order)
-  unsigned long long sortk[SEL_MAXSORT];  // candidates sorted descending
-  double cum[SEL_MAXSORT];
   float qv[D];
   float ps[B];
   int wsum[32];
@@ -354,7 +354,19 @@ struct SelSmem {
   uint32_t krange[2];
   double redd[40];
   float redf[40];
+  union {
+    int hist[2048];                       // radix-select histogram
+    double cum[SEL_MAXSORT];              // coverage prefix (after the sort)
+  } __align__(16);
+  unsigned long long cand[SEL_MAXSORT];   // candidates (block order)
+  unsigned long long sortk[SEL_MAXSORT];  // candidates sorted descending
 };
+__host__ __device__ inline size_t sel_body_bytes(int max_blocks) {
+  const size_t ub = (size_t)2 * H * ((max_blocks + 31) / 32) * 4;  // build_union's bitmaps
+  const size_t need = offsetof(SelSmem, hist) + ub;
+  const size_t body = need > sizeof(SelSmem) ? need : sizeof(SelSmem);
+  return (body + 15) & ~(size_t)15;
+}
 
 // Phase profile of k_select (build with -DCKV_SELPROF; tools/selprof.py): thread 0
 // of every CTA adds globaltimer deltas between barrier-fenced markers.
@@ -381,8 +393,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
 #endif
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SelSmem& S = *reinterpret_cast<SelSmem*>(smem_raw);
-  uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sizeof(SelSmem));
   const ckv_cache& c = a.c;
+  uint32_t* fmask = reinterpret_cast<uint32_t*>(smem_raw + sel_body_bytes(c.max_blocks));
   const ckv_step& st = a.st;
   TraceScope trace_(st.trace, CKV_TR_SELECT);
   const ckv_policy& pol = a.pol;
@@ -944,7 +956,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? SEL_MINB : (NT == 512 ? 2 : 1)
       __threadfence();
     }
     __syncthreads();
-    if (last) build_union(c, st, u, reinterpret_cast<uint32_t*>(&S), S.wsum);
+    if (last) build_union(c, st, u, reinterpret_cast<uint32_t*>(S.hist), S.wsum);
     if (last) SELPROF(9);
     if (last && st.flow) {  // the unit's selection and union list are published
       __threadfence();
@@ -1029,7 +1041,7 @@ static cudaError_t launch_tail(const ckv_cache* c, const ckv_policy* pol, const 
                                const ckv_scratch* sc, int host_max_blocks, int u0, int nu,
                                int nsplit, bool finish, cudaStream_t s) {
   StepArgs a{*c, *st, *pol, PageView{}, u0, 0, nsplit};
-  const size_t smS = sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4;
+  const size_t smS = sel_body_bytes(c->max_blocks) + ((c->max_blocks + 31) / 32) * 4;
   const int nbh = host_max_blocks;  // selection only touches the filled blocks
   // few (unit, head) CTAs (e.g. 8-way KV-head sharding): 1024 threads per head, so
   // each CTA's serial phases are shorter; otherwise 256 threads, 4 CTAs per SM
@@ -1141,10 +1153,11 @@ bool decode_flow(const ckv_cache* c, const ckv_step* st) {
 cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_step* st,
                           const ckv_scratch* sc, int host_max_blocks, bool finish, cudaStream_t s) {
   g_launches = 0;
-  set_max_dyn_smem(k_pass_a<2>, (int)sizeof(PassASmem<2>));
-  set_max_dyn_smem(k_pass_a<3>, (int)sizeof(PassASmem<3>));
+  const size_t smA2 = sizeof(PassASmem<2>), smA3 = sizeof(PassASmem<3>);
+  set_max_dyn_smem(k_pass_a<2>, (int)smA2);
+  set_max_dyn_smem(k_pass_a<3>, (int)smA3);
   {
-    const int smS = (int)(sizeof(SelSmem) + ((c->max_blocks + 31) / 32) * 4);
+    const int smS = (int)(sel_body_bytes(c->max_blocks) + ((c->max_blocks + 31) / 32) * 4);
     set_max_dyn_smem(k_select<8, 1024>, smS);
     set_max_dyn_smem(k_select<16, 1024>, smS);
     set_max_dyn_smem(k_select<32, 1024>, smS);
@@ -1189,11 +1202,9 @@ cudaError_t launch_decode(const ckv_cache* c, const ckv_policy* pol, const ckv_s
       const bool pdl = k == 0 && !st->prof_begin;
       const long long ctas = (long long)max(nsplit_used, 1) * nu;
       if (ctas >= PA_DEEP_WAVES * (long long)dev_state().sms * PA_MINB)
-        e = launch_k(pdl, k_pass_a<3>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32),
-                     sizeof(PassASmem<3>), s, a);
+        e = launch_k(pdl, k_pass_a<3>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32), smA3, s, a);
       else
-        e = launch_k(pdl, k_pass_a<2>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32),
-                     sizeof(PassASmem<2>), s, a);
+        e = launch_k(pdl, k_pass_a<2>, dim3(max(nsplit_used, 1), nu), dim3(PA_WARPS * 32), smA2, s, a);
       ++g_launches;
       if (e != cudaSuccess) break;
     }
