@@ -14,5 +14,6 @@ from .engine import (CertifiedDecoder, HeadStepResult, PendingStep, StepOutput, 
                      run_decode_step, rung3_per_head, rung4_all_heads, rung4_staging_bytes)
 from .errors import EmptyCacheError, PagingError, Tier2UnavailableError
 from .harness import (RunResult, Workload, WorkloadConfig, aggregate_telemetry, dump_line,
-                      generate_workload, gqa_union, run_workload, write_telemetry)
+                      generate_workload, gqa_union, resolve_manifest, run_manifest, run_workload,
+                      write_telemetry)
 from .policy import Certificate, FallbackEvent, PolicyConfig, RungFlags, e_key_bound

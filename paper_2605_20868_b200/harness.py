@@ -331,3 +331,51 @@ def write_telemetry(result, path, config_path="", seed_override=None, version="0
             fh.write(dump_line({"kind": "step", **record}) + "\n")
         fh.write(dump_line({"kind": "summary", **result.summary}) + "\n")
     return path
+
+
+_CONFIG_SECTIONS = {"workload", "policy", "scratch", "seed", "layers"}
+_SCRATCH_FIELDS = {"key_capacity", "value_capacity"}
+
+
+def resolve_manifest(config_path, seed=None):
+    """A run manifest (JSON) resolved as the reference CLI resolves it
+    (cli.py:36-77): the same sections, seed override, scratch defaults of 2048
+    blocks and error messages (``ValueError`` here for the CLI's ConfigError)."""
+    import json
+    from .policy import PolicyConfig
+    try:
+        with open(config_path) as fh:
+            raw = json.load(fh)
+    except OSError as exc:
+        raise ValueError(f"cannot read config: {exc}") from exc
+    except json.JSONDecodeError as exc:
+        raise ValueError(f"malformed JSON at line {exc.lineno}, column {exc.colno}: {exc.msg}") from exc
+    if not isinstance(raw, dict):
+        raise ValueError("config root must be a JSON object")
+    unknown = set(raw) - _CONFIG_SECTIONS
+    if unknown:
+        raise ValueError(f"unknown config sections: {sorted(unknown)}")
+    workload_raw = dict(raw.get("workload", {}))
+    if seed is not None:
+        workload_raw["seed"] = seed
+    elif "seed" in raw:
+        workload_raw.setdefault("seed", raw["seed"])
+    workload = WorkloadConfig.from_dict(workload_raw)
+    policy = PolicyConfig.from_dict(raw.get("policy", {}))
+    scratch = dict(raw.get("scratch", {}))
+    unknown = set(scratch) - _SCRATCH_FIELDS
+    if unknown:
+        raise ValueError(f"unknown scratch fields: {sorted(unknown)}")
+    return (workload, policy, int(scratch.get("key_capacity", 2048)),
+            int(scratch.get("value_capacity", 2048)), int(raw.get("layers", 1)))
+
+
+def run_manifest(config_path, out_path, seed=None):
+    """``certkv run`` (cli.py:98-117) on the device path: resolve the manifest,
+    run the workload, write the bound report (header, one line per step, summary)
+    to ``out_path``.  Returns the RunResult."""
+    workload_cfg, policy, key_cap, value_cap, layers = resolve_manifest(config_path, seed)
+    result = run_workload(generate_workload(workload_cfg), policy, key_capacity=key_cap,
+                          value_capacity=value_cap, layers=layers)
+    write_telemetry(result, out_path, config_path=config_path, seed_override=seed)
+    return result

@@ -229,8 +229,35 @@ def fault_golden():
         tripped_rung4=np.asarray(any(e.rung == 4 for e in tripped.events)))
 
 
+TELEMETRY_MANIFEST = {
+    "workload": {"kind": "gaussian", "n_tokens": 2000, "head_dim": 128, "query_heads": 8,
+                 "kv_heads": 2, "steps": 3, "ingest_binary16": True},
+    "policy": {"exploration_rate": 0.0, "k_max": 24},
+    "scratch": {"key_capacity": 64, "value_capacity": 64},
+    "seed": 17,
+}
+
+
+def telemetry_golden():
+    """The reference CLI's bound report (cli.py:98-117, ``certkv run``) for a fixed
+    manifest: tests/golden/telemetry_manifest.json -> telemetry_ref.jsonl."""
+    from certkv.cli import RunManifest, cmd_run
+    cfg = os.path.join(HERE, "telemetry_manifest.json")
+    with open(cfg, "w") as f:
+        json.dump(TELEMETRY_MANIFEST, f, indent=1, sort_keys=True)
+    # the manifest path is echoed into the header: record it relative to the repo root
+    cwd = os.getcwd()
+    os.chdir(os.path.dirname(os.path.dirname(HERE)))
+    try:
+        cmd_run(RunManifest(config_path="tests/golden/telemetry_manifest.json",
+                            out_path=os.path.join(HERE, "telemetry_ref.jsonl")))
+    finally:
+        os.chdir(cwd)
+
+
 if __name__ == "__main__":
     quantizer_golden()
     workload_golden()
     fault_golden()
+    telemetry_golden()
     print("golden vectors written to", HERE)

@@ -581,3 +581,44 @@ def test_alternate_paths_bit_identical(ck, monkeypatch, env):
         np.testing.assert_array_equal(alt[1][s], base[1][s], err_msg=f"certificates step {s}")
         if base[2][s] is not None:
             np.testing.assert_array_equal(alt[2][s], base[2][s], err_msg=f"page stats step {s}")
+
+
+# ---- the bound report of a run manifest (certkv run, cli.py:98-117) -------------------
+
+def _walk(a, b, path, tol):
+    """Recursive comparison: same keys in the same order, equal integers / booleans /
+    strings, floats within ``tol`` relative (the unmodified reference keeps fp64
+    metadata the device narrows)."""
+    if isinstance(a, dict):
+        assert isinstance(b, dict) and list(a) == list(b), (path, list(a), list(b))
+        for k in a:
+            _walk(a[k], b[k], f"{path}.{k}", tol)
+    elif isinstance(a, list):
+        assert isinstance(b, list) and len(a) == len(b), path
+        for i, (x, y) in enumerate(zip(a, b)):
+            _walk(x, y, f"{path}[{i}]", tol)
+    elif isinstance(a, float) and not isinstance(b, bool):
+        assert isinstance(b, (int, float)), path
+        assert abs(a - b) <= tol * max(abs(a), abs(b)) + 1e-12, (path, a, b)
+    else:
+        assert type(a) is type(b) and a == b, (path, a, b)
+
+
+def test_run_manifest_matches_reference_cli(ck, tmp_path, monkeypatch):
+    """``run_manifest`` on the manifest the golden script ran through the unmodified
+    reference CLI (tests/golden/telemetry_ref.jsonl): the same lines, key sets and key
+    order (sorted, compact JSON), the same header apart from the kernel backend's
+    name, identical decisions, events, rung counts, scratch hits / misses and page-in
+    bytes, certificate floats within the narrowing tolerance."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    monkeypatch.chdir(root)
+    out = str(tmp_path / "run.jsonl")
+    ck.run_manifest("tests/golden/telemetry_manifest.json", out)
+    ref = open(os.path.join(root, "tests", "golden", "telemetry_ref.jsonl")).read().splitlines()
+    dev = open(out).read().splitlines()
+    assert len(dev) == len(ref)
+    r0, d0 = json.loads(ref[0]), json.loads(dev[0])
+    assert r0.pop("kernel_backend") == "pure" and d0.pop("kernel_backend") == "b200"
+    assert d0 == r0
+    for i, (r, d) in enumerate(zip(ref[1:], dev[1:])):
+        _walk(json.loads(r), json.loads(d), f"line{i + 1}", 5e-3)

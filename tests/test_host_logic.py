@@ -131,3 +131,24 @@ def test_scratch_cache_reference_view_and_page_report():
     assert (s.hits, s.misses, s.bytes_paged_in, s.hit_rate) == (3, 1, 4096, 0.75)
     r = PageInReport(2, 1, 4096)
     assert r.to_dict() == {"hits": 2, "misses": 1, "bytes": 4096} and r.payloads == {}
+
+
+def test_resolve_manifest_as_the_reference_cli(tmp_path):
+    """Run manifests resolve as cli.py:36-77 resolves them: sections, seed
+    override, scratch defaults, and the same refusals."""
+    import json
+    from paper_2605_20868_b200.harness import resolve_manifest
+    p = tmp_path / "m.json"
+    p.write_text(json.dumps({"workload": {"kind": "gaussian", "n_tokens": 100, "head_dim": 128,
+                                          "ingest_binary16": True}, "seed": 9,
+                             "policy": {"k_max": 8}, "scratch": {"key_capacity": 32}}))
+    wl, pol, kc, vc, layers = resolve_manifest(str(p))
+    assert (wl.seed, pol.k_max, kc, vc, layers) == (9, 8, 32, 2048, 1)
+    assert resolve_manifest(str(p), seed=3)[0].seed == 3
+    for bad in ({"extra": {}}, {"scratch": {"slots": 1}}, {"workload": {"nope": 1}}, []):
+        p.write_text(json.dumps(bad))
+        with pytest.raises(ValueError):
+            resolve_manifest(str(p))
+    p.write_text("{")
+    with pytest.raises(ValueError, match="malformed JSON"):
+        resolve_manifest(str(p))
